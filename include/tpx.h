@@ -1,0 +1,135 @@
+/* tpx.h — C ABI of the B200-native executor for tileplan execution plans.
+ *
+ * Drop-in replacement for the reference's hot path, the CPU plan executor
+ *   NumericCheck execute_numeric(const ExecutionPlan&, uint64_t seed [, FunctionBindings])
+ *       (reference: proj/include/tileplan/simulator.hpp:43-45, proj/src/simulator.cpp:55-149)
+ * and its per-sub-op kernels / region movers
+ *   run_op_dense, extract_region, paste_region   (proj/include/tileplan/dense.hpp:40-49)
+ * consuming the reference planner's plan exactly as serialised by
+ *   std::string export_plan(const ExecutionPlan&)  (proj/include/tileplan/execgraph.hpp:57,
+ *                                                   proj/src/execgraph.cpp:323-361)
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.  Every entry
+ * point returns 0 on success and a non-zero status on failure, with the message (naming the
+ * offending node / tensor / op, like tileplan::Error, proj/include/tileplan/error.hpp:8-12)
+ * available from tpx_last_error() on the calling thread.  Nothing throws across the ABI.
+ *
+ * Process model: one process per GPU.  A plan with 2^k logical devices is executed by `world`
+ * ranks; logical device d belongs to rank (d * world) >> k (contiguous blocks).  With world=1
+ * a single GPU hosts every logical device (fetches become HBM copies).  Cross-rank fetches
+ * are grouped per plan phase into NCCL send/recv groups (the communicator is created from a
+ * 128-byte ncclUniqueId the caller distributes, e.g. with torch.distributed).
+ */
+#ifndef TPX_H_
+#define TPX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPX_OK 0
+#define TPX_ERR 1
+
+/* Arithmetic of the per-GPU sub-op kernels. */
+#define TPX_PREC_TF32 0   /* fp32 storage, tcgen05 kind::tf32 MMA, fp32 accumulate   */
+#define TPX_PREC_FP32 1   /* fp32 storage, 3xTF32 split MMA (fp32-accurate products) */
+
+/* tpx_plan_stats() keys */
+typedef struct tpx_stats {
+  int64_t fetch_bytes_total;      /* sum of fetch.bytes over the whole plan (all devices) */
+  int64_t rank_fetch_bytes_in;    /* fetch bytes landing on this rank's devices          */
+  int64_t rank_xrank_bytes_in;    /* ... of which cross a rank boundary (NCCL)           */
+  int64_t rank_xrank_bytes_out;   /* bytes this rank sends to other ranks                */
+  int64_t n_nodes;                /* plan nodes (all devices)                            */
+  int64_t n_steps;                /* lowered launch steps on this rank                   */
+  int64_t n_kernel_launches;      /* kernels per tpx_execute on this rank                */
+  int64_t n_gemm_launches;
+  int64_t n_copy_launches;
+  int64_t n_nccl_groups;
+  int64_t n_fused_ew;             /* elementwise sub-ops folded into a GEMM epilogue      */
+  int64_t device_bytes;           /* HBM arena bytes allocated for node values           */
+  double gemm_flops;              /* 2*M*N*K over this rank's matmul sub-ops             */
+  double gemm_min_bytes;          /* operand + output bytes of those GEMMs (read once)   */
+} tpx_stats;
+
+const char* tpx_last_error(void);
+int tpx_version(void);
+
+/* ---------------------------------------------------------------- context */
+typedef struct tpx_ctx tpx_ctx;
+
+/* cuda_ordinal < 0 creates a host-only context: plans can be loaded, validated and lowered
+ * (message tables, byte accounting) without a GPU, but not executed. */
+int tpx_create(int cuda_ordinal, int rank, int world, tpx_ctx** out);
+/* Multi-rank: create the NCCL communicator (world > 1).  `unique_id` is 128 bytes. */
+int tpx_init_comm(tpx_ctx* ctx, const void* unique_id, size_t len);
+/* Writes a fresh 128-byte ncclUniqueId (rank 0 calls this, then broadcasts it). */
+int tpx_comm_unique_id(void* out, size_t len);
+int tpx_destroy(tpx_ctx* ctx);
+
+/* ---------------------------------------------------------------- plans */
+typedef struct tpx_plan tpx_plan;
+
+/* Parse + validate + lower a plan document (export_plan JSON, execgraph.cpp:323-361) for this
+ * context's rank.  flags: bit0 = fuse elementwise sub-ops into GEMM epilogues (default on
+ * when set), bit1 = route every cross-logical-device fetch through the NCCL path even when
+ * both devices live on this rank (self send/recv; exercises the multi-rank data path on one
+ * GPU). */
+#define TPX_FLAG_FUSE 1
+#define TPX_FLAG_FORCE_XCHG 2
+int tpx_load_plan(tpx_ctx* ctx, const char* plan_json, size_t len, int precision, int flags,
+                  tpx_plan** out);
+int tpx_plan_free(tpx_plan* plan);
+int tpx_plan_stats(const tpx_plan* plan, tpx_stats* out);
+/* Lowered program as JSON (steps, per-phase message tables, byte counts) — host-only. */
+int tpx_plan_describe(const tpx_plan* plan, char** json_out);
+void tpx_free_string(char* s);
+
+/* Fill every graph input's buffer node on this rank with seeded_tensor values
+ * (proj/src/dense.cpp:49-57: splitmix64 keyed by seed ^ FNV-1a(tensor id), U[-1,1) in fp64,
+ * rounded to fp32), generated on the GPU for exactly the node's region. */
+int tpx_init_inputs(tpx_plan* plan, uint64_t seed);
+
+/* Node values on this rank (fp64 host buffers, row-major over the node's region). */
+int tpx_node_elements(const tpx_plan* plan, const char* node_id, int64_t* n);
+int tpx_write_node(tpx_plan* plan, const char* node_id, const double* src, int64_t n);
+int tpx_read_node(tpx_plan* plan, const char* node_id, double* dst, int64_t n);
+/* fp32 host <-> device for a node (pinned buffers give async copies on the plan stream). */
+int tpx_write_node_f32(tpx_plan* plan, const char* node_id, const float* src, int64_t n);
+int tpx_read_node_f32(tpx_plan* plan, const char* node_id, float* dst, int64_t n);
+/* Device address + element strides of a node value (for zero-copy interop). */
+int tpx_node_view(const tpx_plan* plan, const char* node_id, uint64_t* dev_ptr, int* rank,
+                  int64_t* shape4, int64_t* strides4);
+
+/* Stream the plan's kernels are enqueued on (0 = the context's own stream). */
+int tpx_set_stream(tpx_plan* plan, uint64_t cuda_stream);
+/* Execute every lowered step once (asynchronous on the plan stream). */
+int tpx_execute(tpx_plan* plan);
+/* Execute only the steps of the given op id (teacher-forced per-op checks). */
+int tpx_execute_op(tpx_plan* plan, const char* op_id);
+/* Loop carry: after a train step, copy each `<w>_next` tensor's holder blocks onto `<w>`'s
+ * holder blocks (conversion between their tilings, fetching across devices as needed). */
+int tpx_carry_weights(tpx_plan* plan);
+int tpx_synchronize(tpx_plan* plan);
+
+/* Per-step device timing of the last tpx_execute (events around each step): total ms and
+ * ms spent in GEMM launches. */
+int tpx_last_timing(const tpx_plan* plan, double* total_ms, double* gemm_ms, double* copy_ms);
+int tpx_enable_timing(tpx_plan* plan, int on);
+
+/* ---------------------------------------------------------------- kernel-level entry points
+ * Device pointers (fp32).  Used by the kernel tests; the plan executor calls the same code.
+ * out = op(A) . op(B) (run_matmul, dense.cpp:71-90); a/b are row-major views with row
+ * strides (elements).  epi_* optionally chain elementwise stages onto the product. */
+int tpx_gemm(const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs, const float* b,
+             int64_t b_rows, int64_t b_cols, int64_t b_rs, int transpose_a, int transpose_b,
+             float* c, int64_t c_rs, int n_epi, const int* epi_ops, const float* epi_scales,
+             const float* const* epi_other, const int64_t* epi_other_rs, float* const* epi_out,
+             const int64_t* epi_out_rs, uint64_t cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPX_H_ */

@@ -1,0 +1,121 @@
+"""ctypes binding of the native library (include/tpx.h).
+
+The library is built in-tree by `paper_1805_04170_b200/build.py` (or `__graft_entry__.build()`).
+There is no fallback: if `_lib/libtpx.so` is missing, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "_lib", "libtpx.so")
+
+_lib = None
+
+P = ctypes.POINTER
+c_i64, c_int, c_u64, c_dbl, c_vp, c_char_p = (ctypes.c_int64, ctypes.c_int, ctypes.c_uint64,
+                                              ctypes.c_double, ctypes.c_void_p, ctypes.c_char_p)
+
+
+class TpxError(RuntimeError):
+    """An error reported by the native library (mirrors tileplan::Error)."""
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("fetch_bytes_total", c_i64), ("rank_fetch_bytes_in", c_i64),
+        ("rank_xrank_bytes_in", c_i64), ("rank_xrank_bytes_out", c_i64), ("n_nodes", c_i64),
+        ("n_steps", c_i64), ("n_kernel_launches", c_i64), ("n_gemm_launches", c_i64),
+        ("n_copy_launches", c_i64), ("n_nccl_groups", c_i64), ("n_fused_ew", c_i64),
+        ("device_bytes", c_i64), ("gemm_flops", c_dbl), ("gemm_min_bytes", c_dbl),
+    ]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+# Declared signatures: name -> (argtypes).  restype is int (status) unless noted.
+_SIGS = {
+    "tpx_version": [],
+    "tpx_create": [c_int, c_int, c_int, P(c_vp)],
+    "tpx_init_comm": [c_vp, c_vp, ctypes.c_size_t],
+    "tpx_comm_unique_id": [c_vp, ctypes.c_size_t],
+    "tpx_destroy": [c_vp],
+    "tpx_load_plan": [c_vp, c_char_p, ctypes.c_size_t, c_int, c_int, P(c_vp)],
+    "tpx_plan_free": [c_vp],
+    "tpx_plan_stats": [c_vp, P(Stats)],
+    "tpx_plan_describe": [c_vp, P(c_vp)],
+    "tpx_init_inputs": [c_vp, c_u64],
+    "tpx_node_elements": [c_vp, c_char_p, P(c_i64)],
+    "tpx_write_node": [c_vp, c_char_p, P(c_dbl), c_i64],
+    "tpx_read_node": [c_vp, c_char_p, P(c_dbl), c_i64],
+    "tpx_write_node_f32": [c_vp, c_char_p, c_vp, c_i64],
+    "tpx_read_node_f32": [c_vp, c_char_p, c_vp, c_i64],
+    "tpx_node_view": [c_vp, c_char_p, P(c_u64), P(c_int), P(c_i64), P(c_i64)],
+    "tpx_set_stream": [c_vp, c_u64],
+    "tpx_execute": [c_vp],
+    "tpx_execute_op": [c_vp, c_char_p],
+    "tpx_carry_weights": [c_vp],
+    "tpx_synchronize": [c_vp],
+    "tpx_last_timing": [c_vp, P(c_dbl), P(c_dbl), P(c_dbl)],
+    "tpx_enable_timing": [c_vp, c_int],
+    "tpx_gemm": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_i64,
+                 c_int, P(c_int), P(ctypes.c_float), P(c_vp), P(c_i64), P(c_vp), P(c_i64), c_u64],
+}
+
+
+def exported_symbols():
+    """Every entry point include/tpx.h declares (used by the symbol-export test)."""
+    return sorted(list(_SIGS) + ["tpx_last_error", "tpx_free_string"])
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise TpxError(f"native library missing: {LIB_PATH} — run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        L.tpx_last_error.restype = c_char_p
+        if hasattr(L, "tpx_free_string"):
+            L.tpx_free_string.argtypes = [c_vp]
+            L.tpx_free_string.restype = None
+        for name, args in _SIGS.items():
+            if not hasattr(L, name):
+                continue  # reported by the export test; calling it raises AttributeError
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = c_int
+        _lib = L
+    return _lib
+
+
+def check(status: int):
+    if status != 0:
+        raise TpxError(lib().tpx_last_error().decode())
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None):
+    """C = op(A) @ op(B) on the tcgen05 path; A, B, C are 2-D fp32 CUDA tensors with unit
+    inner stride.  `epi` = [(op, scale, other_or_None, out), ...] (gemm.h EpiOp codes)."""
+    import torch  # plumbing only: device pointers and the current stream
+
+    for t in (A, B, C):
+        if t.dtype != torch.float32 or t.dim() != 2 or t.stride(1) != 1:
+            raise TpxError("gemm operands must be 2-D fp32 with unit inner stride")
+    epi = epi or []
+    n = len(epi)
+    ops = (c_int * max(n, 1))(*[e[0] for e in epi])
+    scales = (ctypes.c_float * max(n, 1))(*[e[1] for e in epi])
+    others = (c_vp * max(n, 1))(*[(e[2].data_ptr() if e[2] is not None else 0) for e in epi])
+    others_rs = (c_i64 * max(n, 1))(*[(e[2].stride(0) if e[2] is not None else 0) for e in epi])
+    outs = (c_vp * max(n, 1))(*[e[3].data_ptr() for e in epi])
+    outs_rs = (c_i64 * max(n, 1))(*[e[3].stride(0) for e in epi])
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    check(lib().tpx_gemm(_ptr(A), A.shape[0], A.shape[1], A.stride(0), _ptr(B), B.shape[0],
+                         B.shape[1], B.stride(0), int(ta), int(tb), _ptr(C), C.stride(0), n, ops,
+                         scales, others, others_rs, outs, outs_rs, s))

@@ -1,0 +1,126 @@
+"""GPU smoke + micro-benchmark of the tcgen05 GEMM through the C ABI (tpx_gemm).
+
+    python tools/gemm_check.py [--bench]
+Compares against torch fp64 matmul of the same fp32 inputs: normwise error
+max|d| / max|ref| must be <= 2e-3 (TF32 inputs, fp32 accumulate).
+"""
+import ctypes
+import os
+import sys
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1805_04170_b200 import native  # noqa: E402
+
+
+def run(M, N, K, ta, tb, epi=None, pad=0):
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(M * 7 + N * 3 + K)
+    A = torch.rand((K, M) if ta else (M, K), device=dev, generator=g) * 2 - 1
+    B = torch.rand((N, K) if tb else (K, N), device=dev, generator=g) * 2 - 1
+    if pad:
+        A = torch.nn.functional.pad(A, (0, pad))[:, : A.shape[1]]
+    C = torch.full((M, N), float("nan"), device=dev)
+    outs = []
+    if epi:
+        for op in epi:
+            outs.append(torch.full((M, N), float("nan"), device=dev))
+    W = torch.rand((M, N), device=dev, generator=g) * 2 - 1
+    native.gemm(A, B, ta, tb, C, epi=[(op, 0.01, W if op >= 4 else None, o) for op, o in zip(epi or [], outs)])
+    torch.cuda.synchronize()
+    ref = (A.double().T if ta else A.double()) @ (B.double().T if tb else B.double())
+    err = ((C.double() - ref).abs().max() / ref.abs().max()).item()
+    res = [err]
+    prev = ref
+    for op, o in zip(epi or [], outs):
+        if op == 1:
+            prev = torch.tanh(prev)
+        elif op == 2:
+            prev = 1 - torch.tanh(prev) ** 2
+        elif op == 3:
+            prev = 0.01 * prev
+        elif op == 5:
+            prev = prev - W.double()
+        elif op == 6:
+            prev = W.double() - prev
+        res.append(((o.double() - prev).abs().max() / prev.abs().max().clamp_min(1e-30)).item())
+    return res
+
+
+def bench(M, N, K, ta, tb, iters=20):
+    A = torch.rand((K, M) if ta else (M, K), device="cuda")
+    B = torch.rand((N, K) if tb else (K, N), device="cuda")
+    C = torch.empty((M, N), device="cuda")
+    for _ in range(3):
+        native.gemm(A, B, ta, tb, C)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        native.gemm(A, B, ta, tb, C)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / iters
+    tf = 2 * M * N * K / ms / 1e9
+    gb = 4 * (M * K + K * N + M * N) / ms / 1e6
+    return ms, tf, gb
+
+
+def diag():
+    import ctypes
+    L = native.lib()
+    for lbo, sbo in [(4096, 512), (512, 4096), (4096, 1024), (1024, 4096)]:
+        L.tpx_debug_gemm_mn_desc(ctypes.c_uint(lbo), ctypes.c_uint(sbo))
+        for c in [(128, 128, 32, False, False), (128, 128, 8, False, False), (256, 256, 64, True, False)]:
+            M, N, K, ta, tb = c
+            A = torch.rand((K, M) if ta else (M, K), device="cuda") * 2 - 1
+            B = torch.rand((N, K) if tb else (K, N), device="cuda") * 2 - 1
+            C = torch.full((M, N), float("nan"), device="cuda")
+            native.gemm(A, B, ta, tb, C)
+            ref = (A.double().T if ta else A.double()) @ (B.double().T if tb else B.double())
+            err = ((C.double() - ref).abs().max() / ref.abs().max()).item()
+            print(f"lbo={lbo} sbo={sbo} case={c} err={err:.3g} nan={C.isnan().sum().item()} "
+                  f"zeros={(C == 0).sum().item()} cmax={C.abs().max().item():.3g} refmax={ref.abs().max().item():.3g}")
+            if K == 8 and lbo == 4096:
+                r = ref.float()
+                print("  C[0,:4]", C[0, :4].tolist(), " ref[0,:4]", r[0, :4].tolist())
+    L.tpx_debug_gemm_mn_desc(ctypes.c_uint(0), ctypes.c_uint(0))
+
+
+def main():
+    if "--diag" in sys.argv:
+        diag()
+    cases = [
+        (128, 128, 32, False, False), (128, 256, 64, False, True), (256, 256, 256, True, False),
+        (512, 1024, 1024, False, False), (512, 1024, 1024, False, True), (1024, 1024, 512, True, False),
+        (64, 1024, 1024, False, False), (64, 1024, 1024, False, True), (32, 2048, 4096, False, False),
+        (4, 4096, 4096, False, False), (200, 300, 100, False, False), (1000, 136, 72, True, True),
+        (64, 1000, 4096, False, False), (16, 1000, 1024, False, True),
+    ]
+    ok = True
+    for c in cases:
+        errs = run(*c)
+        good = all(e <= 2e-3 for e in errs)
+        ok &= good
+        print(f"{'ok ' if good else 'BAD'} M,N,K,ta,tb={c} err={errs}")
+    for epi in ([1, 2], [3, 6], [1]):
+        errs = run(512, 512, 256, False, False, epi=epi)
+        good = all(e <= 2e-3 for e in errs)
+        ok &= good
+        print(f"{'ok ' if good else 'BAD'} epilogue {epi} err={errs}")
+    errs = run(32, 512, 512, False, False, epi=[3, 6])
+    print(f"{'ok ' if all(e <= 2e-3 for e in errs) else 'BAD'} swapped epilogue err={errs}")
+    if "--bench" in sys.argv:
+        for c in [(512, 8192, 8192, False, False), (512, 8192, 8192, False, True),
+                  (8192, 8192, 512, True, False), (64, 8192, 8192, False, False),
+                  (4096, 4096, 4096, False, False), (8192, 8192, 8192, False, True)]:
+            ms, tf, gb = bench(*c)
+            print(f"bench {c}: {ms:.3f} ms  {tf:.1f} TFLOP/s  {gb:.0f} GB/s(min bytes)")
+    print("ALL OK" if ok else "FAILURES")
+
+
+if __name__ == "__main__":
+    main()
