@@ -127,7 +127,9 @@ int tpx_gemm(const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs, const
              int64_t b_rows, int64_t b_cols, int64_t b_rs, int transpose_a, int transpose_b,
              float* c, int64_t c_rs, int n_epi, const int* epi_ops, const float* epi_scales,
              const float* const* epi_other, const int64_t* epi_other_rs, float* const* epi_out,
-             const int64_t* epi_out_rs, uint64_t cuda_stream);
+             const int64_t* epi_out_rs, int precision, uint64_t cuda_stream);
+/* Debug: override the MN-major UMMA descriptor strides (bytes; 0 = defaults). */
+int tpx_debug_gemm_mn_desc(unsigned lbo, unsigned sbo);
 
 #ifdef __cplusplus
 }

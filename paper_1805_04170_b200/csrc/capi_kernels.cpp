@@ -24,7 +24,7 @@ __attribute__((visibility("default"))) int tpx_gemm(
     const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs, const float* b, int64_t b_rows,
     int64_t b_cols, int64_t b_rs, int transpose_a, int transpose_b, float* c, int64_t c_rs,
     int n_epi, const int* epi_ops, const float* epi_scales, const float* const* epi_other,
-    const int64_t* epi_other_rs, float* const* epi_out, const int64_t* epi_out_rs,
+    const int64_t* epi_other_rs, float* const* epi_out, const int64_t* epi_out_rs, int precision,
     uint64_t cuda_stream) {
   return tpx::guard([&] {
     if (n_epi < 0 || n_epi > tpx::kMaxEpi) tpx::fail("tpx_gemm: too many epilogue stages");
@@ -50,7 +50,7 @@ __attribute__((visibility("default"))) int tpx_gemm(
     int dev = 0, sms = 148;
     CUDA_CHECK(cudaGetDevice(&dev));
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    tpx::GemmLaunch g = tpx::gemm_prepare({s}, sms);
+    tpx::GemmLaunch g = tpx::gemm_prepare({s}, sms, precision == 1);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
     try {
       tpx::gemm_run(g, st);

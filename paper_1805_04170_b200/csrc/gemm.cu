@@ -27,10 +27,22 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
 
-__host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? 4 : (bn >= 128 ? 6 : 8); }
-__host__ __device__ constexpr uint32_t stage_bytes(int bn) { return uint32_t(BM * BK * 4 + bn * BK * 4); }
-constexpr size_t smem_for(int bn) {
-  return size_t(stages_for(bn)) * stage_bytes(bn) + 1024 + 256;
+// Operand bytes of one k-block; a split (3xTF32) stage also holds the low parts.
+__host__ __device__ constexpr uint32_t operand_bytes(int bn) { return uint32_t(BM * BK * 4 + bn * BK * 4); }
+__host__ __device__ constexpr uint32_t stage_bytes(int bn, bool split) {
+  return operand_bytes(bn) * (split ? 2u : 1u);
+}
+__host__ __device__ constexpr int stages_for(int bn, bool split) {
+  return int((192u * 1024u) / stage_bytes(bn, split)) > 8 ? 8 : int((192u * 1024u) / stage_bytes(bn, split));
+}
+constexpr size_t smem_for(int bn, bool split) {
+  return size_t(stages_for(bn, split)) * stage_bytes(bn, split) + 1024 + 256;
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
 }
 
 __device__ __forceinline__ float epi_apply(int op, float prev, float other, float s) {
@@ -87,12 +99,16 @@ __device__ __forceinline__ void load_chunk(const float* base, long long rs, long
   }
 }
 
-template <int BN, bool P_MN, bool Q_MN>
+// SPLIT = 3xTF32: every fp32 operand x = hi + lo with hi = tf32_rna(x), lo = x - hi (exact);
+// D += lo_A*hi_B + hi_A*lo_B + hi_A*hi_B.  The split is done in shared memory by warps 2..7
+// (idle during the mainloop) between the TMA landing and the MMA issue.
+template <int BN, bool P_MN, bool Q_MN, bool SPLIT>
 __global__ void __launch_bounds__(256, 1)
     gemm_tf32_kernel(const GemmProblem* __restrict__ probs, int nprob) {
-  constexpr int STAGES = stages_for(BN);
+  constexpr int STAGES = stages_for(BN, SPLIT);
   constexpr uint32_t A_BYTES = BM * BK * 4;
-  constexpr uint32_t STAGE = stage_bytes(BN);
+  constexpr uint32_t OPB = operand_bytes(BN);
+  constexpr uint32_t STAGE = stage_bytes(BN, SPLIT);
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
   constexpr uint32_t IDESC = (1u << 4)                 // D format f32
                              | (2u << 7) | (2u << 10)  // A, B format tf32
@@ -104,7 +120,8 @@ __global__ void __launch_bounds__(256, 1)
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
+  uint64_t* split_done = empty + STAGES;
+  uint64_t* tmem_full = split_done + STAGES;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
@@ -126,6 +143,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&split_done[s], 6);  // one arrival per splitting warp
     }
     mbar_init(tmem_full, 1);
     fence_barrier_init();
@@ -147,7 +165,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&empty[s], ph ^ 1);
       uint8_t* sa = smem + s * STAGE;
       uint8_t* sb = sa + A_BYTES;
-      mbar_arrive_expect_tx(&full[s], STAGE);
+      mbar_arrive_expect_tx(&full[s], OPB);
       const int k0 = (kb0 + i) * BK;
       if constexpr (!P_MN) {
         tma_load_2d(sa, pr.tmap_a, &full[s], k0, p0);
@@ -167,7 +185,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 0; i < nkb; ++i) {
       const int s = i % STAGES;
       const uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(&full[s], ph);
+      if constexpr (SPLIT) mbar_wait(&split_done[s], ph);
+      else mbar_wait(&full[s], ph);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE);
       const uint32_t sb = sa + A_BYTES;
@@ -180,12 +199,42 @@ __global__ void __launch_bounds__(256, 1)
                                  : umma_desc(sa + kk * 32, 16, 1024, 2);
         const uint64_t bd = Q_MN ? umma_desc(sb + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1)
                                  : umma_desc(sb + kk * 32, 16, 1024, 2);
-        mma_tf32(tmem_base, ad, bd, IDESC, (i > 0 || kk > 0) ? 1u : 0u);
+        if constexpr (SPLIT) {
+          // low parts live OPB bytes after the high parts, in the same (swizzled) layout
+          const uint64_t lo = uint64_t((OPB >> 4) & 0x3FFFu);
+          mma_tf32(tmem_base, ad + lo, bd, IDESC, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_tf32(tmem_base, ad, bd + lo, IDESC, 1u);
+          mma_tf32(tmem_base, ad, bd, IDESC, 1u);
+        } else {
+          mma_tf32(tmem_base, ad, bd, IDESC, (i > 0 || kk > 0) ? 1u : 0u);
+        }
       }
       mma_commit(&empty[s]);
     }
     mma_commit(tmem_full);
-  } else if (warp >= 4) {
+  }
+  if (SPLIT && warp >= 2) {
+    // ---------------- 3xTF32 split: hi in place, lo into the stage's second half
+    const int tid = threadIdx.x - 64;  // 0..191
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % STAGES;
+      const uint32_t ph = (i / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      float4* hi = reinterpret_cast<float4*>(smem + s * STAGE);
+      float4* lo = reinterpret_cast<float4*>(smem + s * STAGE + OPB);
+      for (int c = tid; c < int(OPB / 16); c += 192) {
+        float4 x = hi[c], h, l;
+        h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
+        l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+        hi[c] = h;
+        lo[c] = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&split_done[s]);
+    }
+  }
+  if (warp >= 4) {
     // ---------------- epilogue warpgroup
     const int ew = warp - 4;
     const int row = ew * 32 + lane;
@@ -271,20 +320,20 @@ done:
 
 using KernelFn = void (*)(const GemmProblem*, int);
 
-template <int BN>
+template <int BN, bool SPLIT>
 KernelFn pick(bool p_mn, bool q_mn) {
-  if (!p_mn && !q_mn) return gemm_tf32_kernel<BN, false, false>;
-  if (!p_mn && q_mn) return gemm_tf32_kernel<BN, false, true>;
-  if (p_mn && !q_mn) return gemm_tf32_kernel<BN, true, false>;
-  return gemm_tf32_kernel<BN, true, true>;
+  if (!p_mn && !q_mn) return gemm_tf32_kernel<BN, false, false, SPLIT>;
+  if (!p_mn && q_mn) return gemm_tf32_kernel<BN, false, true, SPLIT>;
+  if (p_mn && !q_mn) return gemm_tf32_kernel<BN, true, false, SPLIT>;
+  return gemm_tf32_kernel<BN, true, true, SPLIT>;
 }
 
-KernelFn kernel_for(int bn, bool p_mn, bool q_mn) {
+KernelFn kernel_for(int bn, bool p_mn, bool q_mn, bool split) {
   switch (bn) {
-    case 32: return pick<32>(p_mn, q_mn);
-    case 64: return pick<64>(p_mn, q_mn);
-    case 128: return pick<128>(p_mn, q_mn);
-    case 256: return pick<256>(p_mn, q_mn);
+    case 32: return split ? pick<32, true>(p_mn, q_mn) : pick<32, false>(p_mn, q_mn);
+    case 64: return split ? pick<64, true>(p_mn, q_mn) : pick<64, false>(p_mn, q_mn);
+    case 128: return split ? pick<128, true>(p_mn, q_mn) : pick<128, false>(p_mn, q_mn);
+    case 256: return split ? pick<256, true>(p_mn, q_mn) : pick<256, false>(p_mn, q_mn);
   }
   throw std::runtime_error("gemm: unsupported tile width " + std::to_string(bn));
 }
@@ -346,9 +395,10 @@ bool gemm_view_ok(const MatView& v) {
   return true;
 }
 
-GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms) {
+GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool split) {
   if (specs.empty()) throw std::runtime_error("gemm: empty batch");
   GemmLaunch g;
+  g.split = split;
   const GemmSpec& s0 = specs[0];
   const long long M0 = s0.ta ? s0.a.cols : s0.a.rows;
   const long long N0 = s0.tb ? s0.b.rows : s0.b.cols;
@@ -460,14 +510,14 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms) {
   }
   CUDA_CHECK(cudaMalloc(&g.d_problems, probs.size() * sizeof(GemmProblem)));
   CUDA_CHECK(cudaMemcpy(g.d_problems, probs.data(), probs.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
-  g.smem_bytes = smem_for(g.bn);
-  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn);
+  g.smem_bytes = smem_for(g.bn, split);
+  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, split);
   CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem_bytes)));
   return g;
 }
 
 void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
-  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn);
+  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split);
   fn<<<g.units, 256, g.smem_bytes, stream>>>(static_cast<const GemmProblem*>(g.d_problems), g.nprob);
   CUDA_CHECK(cudaGetLastError());
 }

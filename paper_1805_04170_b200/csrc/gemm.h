@@ -69,6 +69,7 @@ struct GemmSpec {
 
 struct GemmLaunch {
   int bn = 0;
+  bool split = false;           // 3xTF32
   bool p_mn = false, q_mn = false, swap = false;
   int units = 0;
   int nprob = 0;
@@ -88,7 +89,8 @@ struct GemmLaunch {
 bool gemm_view_ok(const MatView& v);
 
 // Builds tensor maps / problem tables (device memory owned by the launch).
-GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms);
+// split = 3xTF32 (fp32-accurate products), else single-pass TF32.
+GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool split = false);
 void gemm_run(const GemmLaunch& g, cudaStream_t stream);
 void gemm_free(GemmLaunch& g);
 // Debug override of the MN-major descriptor strides (0 = defaults).

@@ -1,0 +1,408 @@
+// Batched bandwidth kernels: strided N-ary (copy / reduce / elementwise), seeded init, direct
+// conv.  See kernels.h.  Work is tiled by rows of the (dim-merged) innermost extent so the
+// inner loop is division-free and, when every operand is unit-stride and 16-byte aligned,
+// moves float4s.
+#include "kernels.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "util.h"
+
+namespace tpx {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int64_t kTileUnits = 4096;
+
+__device__ __forceinline__ int find_desc(const int64_t* tile_begin_base, size_t stride_bytes,
+                                         int n, int64_t tile) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    const int64_t tb = *reinterpret_cast<const int64_t*>(
+        reinterpret_cast<const char*>(tile_begin_base) + size_t(mid) * stride_bytes);
+    if (tb <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Row tiling shared by nary / init: rows x inner (units) split into tiles of ~kTileUnits.
+struct RowTiling {
+  int64_t rows, inner, rpt, col_chunk, n_col_chunks;
+};
+
+RowTiling row_tiling(int64_t rows, int64_t inner) {
+  RowTiling t;
+  t.rows = rows;
+  t.inner = inner;
+  if (inner >= kTileUnits) {
+    t.rpt = 1;
+    t.col_chunk = kTileUnits;
+    t.n_col_chunks = (inner + kTileUnits - 1) / kTileUnits;
+  } else {
+    t.rpt = std::max<int64_t>(1, kTileUnits / std::max<int64_t>(inner, 1));
+    t.col_chunk = inner;
+    t.n_col_chunks = 1;
+  }
+  return t;
+}
+
+// ---------------------------------------------------------------- nary
+
+struct NaryDev {
+  NaryDesc d;
+  int64_t rows, inner, rpt, col_chunk, n_col_chunks;
+};
+
+__device__ __forceinline__ float nary_apply(int op, int nin, const float* v, float s) {
+  switch (op) {
+    case NARY_COPY: return v[0];
+    case NARY_SUM: {
+      float a = v[0];
+      for (int i = 1; i < nin; ++i) a += v[i];
+      return a;
+    }
+    case NARY_SUB: return v[0] - v[1];
+    case NARY_SCALE: return s * v[0];
+    case NARY_TANH: return tanhf(v[0]);
+    case NARY_DTANH: {
+      const float t = tanhf(v[0]);
+      return 1.0f - t * t;
+    }
+    default: return v[0];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restrict__ ds, int n) {
+  const int di = find_desc(&ds[0].d.tile_begin, sizeof(NaryDev), n, blockIdx.x);
+  const NaryDev& D = ds[di];
+  const NaryDesc& d = D.d;
+  const int64_t local = int64_t(blockIdx.x) - d.tile_begin;
+  const int64_t rb = local / D.n_col_chunks, cc = local % D.n_col_chunks;
+  const int64_t r0 = rb * D.rpt, r1 = min(D.rows, r0 + D.rpt);
+  const int64_t c0 = cc * D.col_chunk, c1 = min(D.inner, c0 + D.col_chunk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nin = d.nin, op = d.op;
+  for (int64_t r = r0 + warp; r < r1; r += kThreads / 32) {
+    const int64_t i2 = r % d.shape[2];
+    const int64_t t = r / d.shape[2];
+    const int64_t i1 = t % d.shape[1];
+    const int64_t i0 = t / d.shape[1];
+    float* out = d.out + i0 * d.out_st[0] + i1 * d.out_st[1] + i2 * d.out_st[2];
+    const float* in[kMaxIn];
+#pragma unroll
+    for (int k = 0; k < kMaxIn; ++k)
+      if (k < nin) in[k] = d.in[k] + i0 * d.in_st[k][0] + i1 * d.in_st[k][1] + i2 * d.in_st[k][2];
+    if (d.vec == 4) {
+      for (int64_t c = c0 + lane; c < c1; c += 32) {
+        float4 v[kMaxIn];
+#pragma unroll
+        for (int k = 0; k < kMaxIn; ++k)
+          if (k < nin) v[k] = __ldg(reinterpret_cast<const float4*>(in[k]) + c);
+        float4 o;
+        if (op == NARY_ACC) {
+          o = reinterpret_cast<float4*>(out)[c];
+          o.x += v[0].x; o.y += v[0].y; o.z += v[0].z; o.w += v[0].w;
+        } else {
+          float a[kMaxIn];
+#pragma unroll
+          for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? v[k].x : 0.f;
+          o.x = nary_apply(op, nin, a, d.scale);
+#pragma unroll
+          for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? v[k].y : 0.f;
+          o.y = nary_apply(op, nin, a, d.scale);
+#pragma unroll
+          for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? v[k].z : 0.f;
+          o.z = nary_apply(op, nin, a, d.scale);
+#pragma unroll
+          for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? v[k].w : 0.f;
+          o.w = nary_apply(op, nin, a, d.scale);
+        }
+        reinterpret_cast<float4*>(out)[c] = o;
+      }
+    } else {
+      const int64_t os = d.out_st[3];
+      for (int64_t c = c0 + lane; c < c1; c += 32) {
+        float a[kMaxIn];
+#pragma unroll
+        for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? __ldg(in[k] + c * d.in_st[k][3]) : 0.f;
+        if (op == NARY_ACC) out[c * os] += a[0];
+        else out[c * os] = nary_apply(op, nin, a, d.scale);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- init (seeded_tensor)
+
+struct InitDev {
+  InitDesc d;
+  int64_t rows, inner, rpt, col_chunk, n_col_chunks;
+};
+
+__device__ __forceinline__ float seeded_value(uint64_t state0, uint64_t flat) {
+  // splitmix64 (dense.cpp:30-36): the i-th draw uses state0 + (i+1)*gamma.
+  uint64_t z = state0 + (flat + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z = z ^ (z >> 31);
+  const uint64_t bits = z >> 11;  // 53 bits
+  const double v = double(bits) * (2.0 / 9007199254740992.0) - 1.0;
+  return float(v);  // round-to-nearest fp64 -> fp32
+}
+
+__global__ void __launch_bounds__(kThreads) init_kernel(const InitDev* __restrict__ ds, int n) {
+  const int di = find_desc(&ds[0].d.tile_begin, sizeof(InitDev), n, blockIdx.x);
+  const InitDev& D = ds[di];
+  const InitDesc& d = D.d;
+  const int64_t local = int64_t(blockIdx.x) - d.tile_begin;
+  const int64_t rb = local / D.n_col_chunks, cc = local % D.n_col_chunks;
+  const int64_t r0 = rb * D.rpt, r1 = min(D.rows, r0 + D.rpt);
+  const int64_t c0 = cc * D.col_chunk, c1 = min(D.inner, c0 + D.col_chunk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t r = r0 + warp; r < r1; r += kThreads / 32) {
+    const int64_t i2 = r % d.ext[2];
+    const int64_t t = r / d.ext[2];
+    const int64_t i1 = t % d.ext[1];
+    const int64_t i0 = t / d.ext[1];
+    const uint64_t rowflat =
+        ((uint64_t(d.lo[0] + i0) * d.full[1] + uint64_t(d.lo[1] + i1)) * d.full[2] +
+         uint64_t(d.lo[2] + i2)) * d.full[3] + uint64_t(d.lo[3]);
+    float* out = d.out + r * d.ext[3];
+    for (int64_t c = c0 + lane; c < c1; c += 32) out[c] = seeded_value(d.state0, rowflat + uint64_t(c));
+  }
+}
+
+// ---------------------------------------------------------------- conv (direct)
+
+__device__ __forceinline__ float at4(const StridedView& v, int64_t a, int64_t b, int64_t c, int64_t d) {
+  return __ldg(v.ptr + a * v.st[0] + b * v.st[1] + c * v.st[2] + d * v.st[3]);
+}
+
+__global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restrict__ ds, int n) {
+  const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
+  const ConvDesc& d = ds[di];
+  const int64_t e = (int64_t(blockIdx.x) - d.tile_begin) * kThreads + threadIdx.x;
+  if (e >= d.n) return;
+  const int64_t o3 = e % d.oshape[3];
+  int64_t t = e / d.oshape[3];
+  const int64_t o2 = t % d.oshape[2];
+  t /= d.oshape[2];
+  const int64_t o1 = t % d.oshape[1];
+  const int64_t o0 = t / d.oshape[1];
+  float acc = 0.f;
+  if (d.mode == CONV_FWD) {
+    // A (n,ci,h,w) x K (co,ci,fh,fw) -> (n,co,ho,wo)
+    const int64_t ci = d.a.shape[1], fh = d.b.shape[2], fw = d.b.shape[3];
+    for (int64_t c = 0; c < ci; ++c)
+      for (int64_t u = 0; u < fh; ++u)
+        for (int64_t v = 0; v < fw; ++v) acc = fmaf(at4(d.a, o0, c, o2 + u, o3 + v), at4(d.b, o1, c, u, v), acc);
+  } else if (d.mode == CONV_GRAD_W) {
+    // A (n,ci,h,w) x G (n,co,ho,wo) -> (co,ci,fh,fw)
+    const int64_t nb = d.a.shape[0], ho = d.b.shape[2], wo = d.b.shape[3];
+    for (int64_t b = 0; b < nb; ++b)
+      for (int64_t y = 0; y < ho; ++y)
+        for (int64_t x = 0; x < wo; ++x) acc = fmaf(at4(d.a, b, o1, y + o2, x + o3), at4(d.b, b, o0, y, x), acc);
+  } else {
+    // G (n,co,ho,wo) x K (co,ci,fh,fw) -> (n,ci,ho+fh-1,wo+fw-1), bounds-checked taps
+    const int64_t co = d.a.shape[1], ho = d.a.shape[2], wo = d.a.shape[3];
+    const int64_t fh = d.b.shape[2], fw = d.b.shape[3];
+    for (int64_t o = 0; o < co; ++o)
+      for (int64_t u = 0; u < fh; ++u) {
+        const int64_t yy = o2 - u;
+        if (yy < 0 || yy >= ho) continue;
+        for (int64_t v = 0; v < fw; ++v) {
+          const int64_t xx = o3 - v;
+          if (xx < 0 || xx >= wo) continue;
+          acc = fmaf(at4(d.a, o0, o, yy, xx), at4(d.b, o, o1, u, v), acc);
+        }
+      }
+  }
+  d.out[e] = acc;
+}
+
+template <class T>
+void upload(std::vector<T>& v, void** dptr) {
+  if (*dptr) cudaFree(*dptr);
+  *dptr = nullptr;
+  if (v.empty()) return;
+  CUDA_CHECK(cudaMalloc(dptr, v.size() * sizeof(T)));
+  CUDA_CHECK(cudaMemcpy(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+}  // namespace
+
+bool StridedView::contiguous() const {
+  int64_t want = 1;
+  for (int i = rank - 1; i >= 0; --i) {
+    if (shape[i] != 1 && st[i] != want) return false;
+    want *= shape[i];
+  }
+  return true;
+}
+
+NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView>& ins, float scale) {
+  if (ins.empty() || int(ins.size()) > kMaxIn) fail("nary: bad operand count");
+  NaryDesc d;
+  std::memset(&d, 0, sizeof d);
+  d.op = op;
+  d.nin = int(ins.size());
+  d.scale = scale;
+  const int r = out.rank;
+  for (const auto& v : ins)
+    for (int i = 0; i < r; ++i)
+      if (v.rank != r || v.shape[i] != out.shape[i]) fail("nary: operand shapes differ");
+  // Collect dims (outer..inner), drop extent-1 dims, merge dims contiguous in every operand.
+  struct Dim {
+    int64_t n, so, si[kMaxIn];
+  };
+  std::vector<Dim> dims;
+  for (int i = 0; i < r; ++i) {
+    if (out.shape[i] == 1) continue;
+    Dim x;
+    x.n = out.shape[i];
+    x.so = out.st[i];
+    for (size_t k = 0; k < ins.size(); ++k) x.si[k] = ins[k].st[i];
+    dims.push_back(x);
+  }
+  std::vector<Dim> merged;
+  for (const auto& x : dims) {
+    if (!merged.empty()) {
+      Dim& p = merged.back();
+      bool ok = p.so == x.so * x.n;
+      for (size_t k = 0; k < ins.size() && ok; ++k) ok = p.si[k] == x.si[k] * x.n;
+      if (ok) {
+        p.n *= x.n;
+        p.so = x.so;
+        for (size_t k = 0; k < ins.size(); ++k) p.si[k] = x.si[k];
+        continue;
+      }
+    }
+    merged.push_back(x);
+  }
+  if (merged.size() > size_t(kMaxRank)) fail("nary: view rank too high after merging");
+  const int pad = kMaxRank - int(merged.size());
+  for (int i = 0; i < kMaxRank; ++i) {
+    if (i < pad) {
+      d.shape[i] = 1;
+      d.out_st[i] = 0;
+      for (size_t k = 0; k < ins.size(); ++k) d.in_st[k][i] = 0;
+    } else {
+      const Dim& x = merged[size_t(i - pad)];
+      d.shape[i] = x.n;
+      d.out_st[i] = x.so;
+      for (size_t k = 0; k < ins.size(); ++k) d.in_st[k][i] = x.si[k];
+    }
+  }
+  d.out = out.ptr;
+  for (size_t k = 0; k < ins.size(); ++k) d.in[k] = ins[k].ptr;
+  // float4 path: unit inner stride everywhere, inner extent % 4, 16B-aligned rows.
+  bool v4 = d.shape[3] % 4 == 0 && d.out_st[3] == 1 && (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
+  for (int i = 0; i < 3 && v4; ++i) v4 = d.out_st[i] % 4 == 0;
+  for (size_t k = 0; k < ins.size() && v4; ++k) {
+    v4 = d.in_st[k][3] == 1 && (reinterpret_cast<uintptr_t>(d.in[k]) & 15) == 0;
+    for (int i = 0; i < 3 && v4; ++i) v4 = d.in_st[k][i] % 4 == 0;
+  }
+  d.vec = v4 ? 4 : 1;
+  d.units = out.elements() / d.vec;
+  return d;
+}
+
+void nary_prepare(NaryBatch& b) {
+  std::vector<NaryDev> dev(b.descs.size());
+  int64_t tiles = 0;
+  b.bytes = 0;
+  for (size_t i = 0; i < b.descs.size(); ++i) {
+    NaryDesc& d = b.descs[i];
+    const int64_t rows = d.shape[0] * d.shape[1] * d.shape[2];
+    const int64_t inner = d.shape[3] / d.vec;
+    RowTiling t = row_tiling(rows, inner);
+    d.tile_begin = tiles;
+    tiles += ((rows + t.rpt - 1) / t.rpt) * t.n_col_chunks;
+    dev[i] = NaryDev{d, t.rows, t.inner, t.rpt, t.col_chunk, t.n_col_chunks};
+    const double elems = double(d.units) * d.vec;
+    b.bytes += 4.0 * elems * (d.nin + 1 + (d.op == NARY_ACC ? 1 : 0));
+  }
+  b.tiles = tiles;
+  upload(dev, &b.d_descs);
+}
+
+void nary_run(const NaryBatch& b, cudaStream_t s) {
+  if (!b.tiles) return;
+  nary_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
+                                                     int(b.descs.size()));
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void nary_free(NaryBatch& b) {
+  if (b.d_descs) cudaFree(b.d_descs);
+  b.d_descs = nullptr;
+}
+
+uint64_t fnv1a(const char* s, size_t n) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= static_cast<unsigned char>(s[i]);
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
+void init_prepare(InitBatch& b) {
+  std::vector<InitDev> dev(b.descs.size());
+  int64_t tiles = 0;
+  for (size_t i = 0; i < b.descs.size(); ++i) {
+    InitDesc& d = b.descs[i];
+    const int64_t rows = d.ext[0] * d.ext[1] * d.ext[2];
+    RowTiling t = row_tiling(rows, d.ext[3]);
+    d.tile_begin = tiles;
+    tiles += ((rows + t.rpt - 1) / t.rpt) * t.n_col_chunks;
+    dev[i] = InitDev{d, t.rows, t.inner, t.rpt, t.col_chunk, t.n_col_chunks};
+  }
+  b.tiles = tiles;
+  upload(dev, &b.d_descs);
+}
+
+void init_run(const InitBatch& b, cudaStream_t s) {
+  if (!b.tiles) return;
+  init_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const InitDev*>(b.d_descs),
+                                                     int(b.descs.size()));
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void init_free(InitBatch& b) {
+  if (b.d_descs) cudaFree(b.d_descs);
+  b.d_descs = nullptr;
+}
+
+void conv_prepare(ConvBatch& b) {
+  int64_t tiles = 0;
+  for (auto& d : b.descs) {
+    d.tile_begin = tiles;
+    tiles += (d.n + kThreads - 1) / kThreads;
+  }
+  b.tiles = tiles;
+  upload(b.descs, &b.d_descs);
+}
+
+void conv_run(const ConvBatch& b, cudaStream_t s) {
+  if (!b.tiles) return;
+  conv_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const ConvDesc*>(b.d_descs),
+                                                     int(b.descs.size()));
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void conv_free(ConvBatch& b) {
+  if (b.d_descs) cudaFree(b.d_descs);
+  b.d_descs = nullptr;
+}
+
+void f32_to_f64_host(const float* src, double* dst, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) dst[i] = double(src[i]);
+}
+
+}  // namespace tpx

@@ -1,0 +1,114 @@
+// Bandwidth kernels of the executor (all batched: one launch per phase step).
+//   nary    strided N-d box copy / accumulate / elementwise over up to 8 operands:
+//           K3 pack/unpack (extract_region / paste_region, dense.cpp:213-259),
+//           K4 partial-sum reduce in source order (reduce_partial, simulator.cpp:106-115),
+//           K5 elementwise sub-ops not folded into a GEMM (run_op_dense, dense.cpp:170-204).
+//   init    K6 seeded inputs on device (seeded_tensor, dense.cpp:30-57), bit-exact fp64 -> fp32.
+//   conv    direct convolution sub-ops (run_conv, dense.cpp:92-157).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace tpx {
+
+constexpr int kMaxRank = 4;
+constexpr int kMaxIn = 8;
+
+enum NaryOp : int {
+  NARY_COPY = 0,   // out = in0
+  NARY_SUM = 1,    // out = in0 + in1 + ... (left to right)
+  NARY_SUB = 2,    // out = in0 - in1
+  NARY_SCALE = 3,  // out = s * in0
+  NARY_TANH = 4,   // out = tanh(in0)
+  NARY_DTANH = 5,  // out = 1 - tanh(in0)^2
+  NARY_ACC = 6,    // out += in0
+};
+
+// A strided fp32 view (element strides), rank <= 4.
+struct StridedView {
+  float* ptr = nullptr;
+  int rank = 0;
+  int64_t shape[kMaxRank] = {1, 1, 1, 1};
+  int64_t st[kMaxRank] = {0, 0, 0, 0};
+  int64_t elements() const {
+    int64_t n = 1;
+    for (int i = 0; i < rank; ++i) n *= shape[i];
+    return n;
+  }
+  bool contiguous() const;
+};
+
+struct NaryDesc {
+  int op = NARY_COPY;
+  int nin = 1;
+  int vec = 1;          // 1 or 4 elements per access
+  float scale = 0.f;
+  int64_t shape[kMaxRank];  // normalised to rank 4 (leading 1s), dims merged where possible
+  float* out;
+  int64_t out_st[kMaxRank];
+  const float* in[kMaxIn];
+  int64_t in_st[kMaxIn][kMaxRank];
+  int64_t tile_begin;   // prefix over the batch (filled by nary_prepare)
+  int64_t units;        // number of vec-wide units
+};
+
+struct NaryBatch {
+  std::vector<NaryDesc> descs;
+  void* d_descs = nullptr;
+  int64_t tiles = 0;
+  double bytes = 0;  // algorithmic bytes moved (reads + writes)
+};
+
+// Build a descriptor: out[i] = op(in_0[i], ...), all views of equal shape.
+NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView>& ins,
+                   float scale = 0.f);
+void nary_prepare(NaryBatch& b);  // uploads descriptor table
+void nary_run(const NaryBatch& b, cudaStream_t s);
+void nary_free(NaryBatch& b);
+
+struct InitDesc {
+  float* out;
+  uint64_t state0;                 // seed ^ fnv1a(tensor id)
+  int rank;
+  int64_t full[kMaxRank];          // full tensor shape (row-major stream order)
+  int64_t lo[kMaxRank];            // region origin
+  int64_t ext[kMaxRank];           // region extent
+  int64_t n;
+  int64_t tile_begin;
+};
+
+struct InitBatch {
+  std::vector<InitDesc> descs;
+  void* d_descs = nullptr;
+  int64_t tiles = 0;
+};
+void init_prepare(InitBatch& b);
+void init_run(const InitBatch& b, cudaStream_t s);
+void init_free(InitBatch& b);
+uint64_t fnv1a(const char* s, size_t n);
+
+enum ConvModeCode : int { CONV_FWD = 0, CONV_GRAD_W = 1, CONV_GRAD_IN = 2 };
+struct ConvDesc {
+  int mode;
+  StridedView a, b;   // rank-4 operands as run_conv receives them
+  float* out;         // contiguous rank-4 output
+  int64_t oshape[4];
+  int64_t n;          // output elements
+  int64_t tile_begin;
+};
+struct ConvBatch {
+  std::vector<ConvDesc> descs;
+  void* d_descs = nullptr;
+  int64_t tiles = 0;
+  double flops = 0;
+};
+void conv_prepare(ConvBatch& b);
+void conv_run(const ConvBatch& b, cudaStream_t s);
+void conv_free(ConvBatch& b);
+
+// fp32 <-> fp64 conversion helpers for host I/O of node values.
+void f32_to_f64_host(const float* src, double* dst, int64_t n);
+
+}  // namespace tpx

@@ -1,0 +1,889 @@
+#include "runtime.h"
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+#include <sstream>
+
+#include "json.h"
+#include "nccl_shim.h"
+#include "util.h"
+
+namespace tpx {
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr uintptr_t kFakeBase = uintptr_t(1) << 40;  // dry-run arena base (256-aligned)
+
+StridedView contiguous_view(float* ptr, const Shape& s) {
+  StridedView v;
+  v.ptr = ptr;
+  v.rank = int(s.size());
+  int64_t st = 1;
+  for (int i = v.rank - 1; i >= 0; --i) {
+    v.shape[i] = s[size_t(i)];
+    v.st[i] = st;
+    st *= s[size_t(i)];
+  }
+  return v;
+}
+
+// Sub-box `sub` of a value covering `vreg`.
+StridedView subview(const StridedView& v, const Region& vreg, const Region& sub) {
+  if (!vreg.contains(sub)) fail("slice region escapes source region");
+  StridedView o = v;
+  int64_t off = 0;
+  for (int i = 0; i < v.rank; ++i) {
+    off += (sub.b[size_t(i)][0] - vreg.b[size_t(i)][0]) * v.st[i];
+    o.shape[i] = sub.b[size_t(i)][1] - sub.b[size_t(i)][0];
+  }
+  o.ptr = v.ptr + off;
+  return o;
+}
+
+MatView mat_view(const StridedView& v) {
+  if (v.rank != 2) fail("matmul operand is not rank 2");
+  MatView m;
+  m.ptr = v.ptr;
+  m.rows = v.shape[0];
+  m.cols = v.shape[1];
+  m.rs = v.st[0];
+  m.cs = v.st[1];
+  if (m.cols == 1) m.cs = 1;  // a single column is unit-stride by definition
+  return m;
+}
+
+// Classes of an open segment, flushed in this order (each may read values produced by an
+// earlier class of the same segment, never by its own or a later class).
+enum Cls { C_PRE = 0, C_COMPUTE = 1, C_PACK = 2, C_XCHG = 3, C_COPY = 4, C_REDUCE = 5, C_N = 6 };
+
+struct Lowerer {
+  PlanRt& P;
+  Plan& pl;
+  Ctx& C;
+  Program& prog;
+  bool dry;
+  bool fuse, force_xchg;
+
+  std::vector<int> consumers;
+  std::vector<int> defer_to;   // concat node index a fetch/slice is pasted into, or -1
+  std::vector<char> is_holder;
+  std::vector<int> pending;    // open class producing the node, or -1
+  std::map<int, std::pair<int, int>> chain_tail;  // node -> (gemm batch, problem)
+  std::vector<int> gemm_step;  // gemm batch -> step index (-1 while open)
+
+  // open segment
+  NaryBatch o_pre, o_ew, o_pack, o_copy, o_reduce;
+  XchgGroup o_xchg;
+  int o_gemm = -1;             // open gemm batch index
+  ConvBatch o_conv;
+  int o_kind = -1;             // 0 gemm, 1 ew, 2 conv
+  std::string o_op, o_pre_op;
+  std::vector<int> o_nodes[C_N];
+  std::string seg_op;          // op owning the conversion classes (phase prefix)
+
+  Lowerer(PlanRt& p, Program& pr, bool d)
+      : P(p), pl(p.plan), C(*p.ctx), prog(pr), dry(d),
+        fuse(p.flags & 1), force_xchg(p.flags & 2) {}
+
+  float* alloc_bytes(size_t bytes) {
+    const size_t off = (P.arena_used + kAlign - 1) / kAlign * kAlign;
+    P.arena_used = off + std::max<size_t>(bytes, 4);
+    if (!dry && P.arena_used > P.arena_bytes) fail("arena overflow (lowering is not deterministic)");
+    return reinterpret_cast<float*>(P.base + off);
+  }
+  StridedView alloc(const Shape& s) {
+    int64_t n = 1;
+    for (auto e : s) n *= e;
+    return contiguous_view(alloc_bytes(size_t(n) * 4), s);
+  }
+
+  int rank_of(int dev) const { return P.dev_rank[size_t(dev)]; }
+  bool mine_dev(int dev) const { return rank_of(dev) == C.rank; }
+
+  int add_step(StepKind k, int idx, const std::string& op, const std::string& what) {
+    prog.steps.push_back(Step{k, idx, op, what});
+    return int(prog.steps.size()) - 1;
+  }
+
+  void produced(int node, Cls c) {
+    pending[size_t(node)] = c;
+    o_nodes[c].push_back(node);
+  }
+
+  void flush() {
+    auto emit_nary = [&](NaryBatch& b, const std::string& op, const std::string& what, Cls c) {
+      if (b.descs.empty()) return;
+      prog.nary.push_back(std::move(b));
+      b = NaryBatch{};
+      const int s = add_step(ST_NARY, int(prog.nary.size()) - 1, op, what);
+      for (int n : o_nodes[c]) P.avail_step[size_t(n)] = s;
+    };
+    emit_nary(o_pre, o_pre_op, "materialize", C_PRE);
+    if (o_kind == 0) {
+      const int s = add_step(ST_GEMM, o_gemm, o_op, "gemm");
+      gemm_step[size_t(o_gemm)] = s;
+      for (int n : o_nodes[C_COMPUTE]) P.avail_step[size_t(n)] = s;
+    } else if (o_kind == 1) {
+      emit_nary(o_ew, o_op, "elementwise", C_COMPUTE);
+    } else if (o_kind == 2) {
+      prog.conv.push_back(std::move(o_conv));
+      o_conv = ConvBatch{};
+      const int s = add_step(ST_CONV, int(prog.conv.size()) - 1, o_op, "conv");
+      for (int n : o_nodes[C_COMPUTE]) P.avail_step[size_t(n)] = s;
+    }
+    emit_nary(o_pack, seg_op, "pack", C_PACK);
+    if (!o_xchg.x.empty()) {
+      prog.xchg.push_back(std::move(o_xchg));
+      o_xchg = XchgGroup{};
+      const int s = add_step(ST_XCHG, int(prog.xchg.size()) - 1, seg_op, "nccl");
+      for (int n : o_nodes[C_XCHG]) P.avail_step[size_t(n)] = s;
+    }
+    emit_nary(o_copy, seg_op, "copy", C_COPY);
+    emit_nary(o_reduce, seg_op, "reduce", C_REDUCE);
+    for (int c = 0; c < C_N; ++c) {
+      for (int n : o_nodes[c]) pending[size_t(n)] = -1;
+      o_nodes[c].clear();
+    }
+    o_kind = -1;
+    o_gemm = -1;
+    o_op.clear();
+  }
+
+  // Flush when `node`'s value is still being produced by an open class >= c.
+  void need(int node, Cls c) {
+    const int pc = pending[size_t(node)];
+    if (pc >= 0 && pc >= int(c)) flush();
+  }
+
+  const StridedView& value(int node) {
+    if (!P.has_val[size_t(node)])
+      fail("node " + pl.nodes[size_t(node)].id + " has no materialised value on this rank");
+    return P.val[size_t(node)];
+  }
+
+  void set_val(int node, const StridedView& v) {
+    P.val[size_t(node)] = v;
+    P.has_val[size_t(node)] = 1;
+  }
+
+  void ensure_alloc(int node) {
+    if (!P.has_val[size_t(node)]) set_val(node, alloc(pl.nodes[size_t(node)].region.shape()));
+  }
+
+  static std::string op_of_phase(const std::string& phase) {
+    const auto p = phase.rfind(':');
+    return p == std::string::npos ? phase : phase.substr(0, p);
+  }
+
+  // ------------------------------------------------------------ sub_op lowering
+  void lower_sub_op(int ni) {
+    const PlanNode& n = pl.nodes[size_t(ni)];
+    const OpSpec& op = pl.op(n.op);
+    for (int s : n.sources) need(s, C_COMPUTE);
+    if (op.kind == OpKind::generic)
+      fail("op '" + op.id + "': unbound function tag (generic ops have no numeric binding)");
+
+    if (op.kind == OpKind::elementwise && fuse && try_fuse(ni, op)) return;
+
+    const int kind = op.kind == OpKind::matmul ? 0 : op.kind == OpKind::elementwise ? 1 : 2;
+    if (o_kind >= 0 && (o_kind != kind || o_op != op.id)) flush();
+    if (o_kind < 0) {
+      o_kind = kind;
+      o_op = op.id;
+      if (kind == 0) {
+        prog.gemm_specs.emplace_back();
+        gemm_step.push_back(-1);
+        o_gemm = int(prog.gemm_specs.size()) - 1;
+      }
+    }
+    const StridedView out = alloc(n.region.shape());
+    set_val(ni, out);
+    if (op.kind == OpKind::matmul) {
+      GemmSpec s;
+      StridedView a = value(n.sources[0]);
+      StridedView b = value(n.sources[1]);
+      s.a = mat_view(a);
+      s.b = mat_view(b);
+      if (!gemm_view_ok(s.a)) s.a = mat_view(materialize(n.sources[0], op.id));
+      if (!gemm_view_ok(s.b)) s.b = mat_view(materialize(n.sources[1], op.id));
+      s.ta = op.ta;
+      s.tb = op.tb;
+      s.c = out.ptr;
+      s.c_rs = out.st[0];
+      s.c_cs = 1;
+      auto& specs = prog.gemm_specs[size_t(o_gemm)];
+      specs.push_back(s);
+      chain_tail[ni] = {o_gemm, int(specs.size()) - 1};
+      const double M = double(op.ta ? s.a.cols : s.a.rows), K = double(op.ta ? s.a.rows : s.a.cols);
+      const double N = double(op.tb ? s.b.rows : s.b.cols);
+      P.gemm_flops += 2.0 * M * N * K;
+      P.gemm_min_bytes += 4.0 * (M * K + K * N + M * N);
+    } else if (op.kind == OpKind::elementwise) {
+      std::vector<StridedView> ins;
+      for (int s : n.sources) ins.push_back(value(s));
+      int code = NARY_COPY;
+      switch (op.fn) {
+        case EwFn::add: code = NARY_SUM; break;
+        case EwFn::sub: code = NARY_SUB; break;
+        case EwFn::scale: code = NARY_SCALE; break;
+        case EwFn::pointwise_fn: code = NARY_TANH; break;
+        case EwFn::pointwise_fn_grad: code = NARY_DTANH; break;
+      }
+      o_ew.descs.push_back(nary_desc(code, out, ins, float(op.scale)));
+    } else {
+      ConvDesc d;
+      std::memset(&d, 0, sizeof d);
+      d.mode = op.mode == ConvMode::forward ? CONV_FWD : op.mode == ConvMode::grad_weight ? CONV_GRAD_W : CONV_GRAD_IN;
+      d.a = value(n.sources[0]);
+      d.b = value(n.sources[1]);
+      d.out = out.ptr;
+      for (int i = 0; i < 4; ++i) d.oshape[i] = out.shape[i];
+      d.n = out.elements();
+      o_conv.descs.push_back(d);
+      const OpSpec& o = op;
+      (void)o;
+      double contr = 0;
+      if (d.mode == CONV_FWD) contr = double(d.b.shape[1] * d.b.shape[2] * d.b.shape[3]) * double(d.n);
+      else if (d.mode == CONV_GRAD_W) contr = double(d.a.shape[0] * d.b.shape[2] * d.b.shape[3]) * double(d.n);
+      else contr = double(d.a.elements()) * double(d.b.shape[1] * d.b.shape[2] * d.b.shape[3]);
+      o_conv.flops += 2.0 * contr;
+    }
+    produced(ni, C_COMPUTE);
+  }
+
+  StridedView materialize(int node, const std::string& op) {
+    // Packed copy of a view the TMA path cannot address (misaligned column slice).
+    if (!o_pre.descs.empty() && o_pre_op != op) flush();
+    o_pre_op = op;
+    // Rows padded to a multiple of 4 floats: TMA needs 16-byte row strides (the padding
+    // columns lie outside the tensor map and are never read).
+    const StridedView& v = value(node);
+    if (v.rank != 2) fail("matmul operand is not rank 2");
+    const int64_t rows = v.shape[0], cols = v.shape[1], ld = (cols + 3) / 4 * 4;
+    StridedView t = alloc({rows, ld});
+    t.shape[1] = cols;
+    o_pre.descs.push_back(nary_desc(NARY_COPY, t, {v}));
+    return t;
+  }
+
+  bool try_fuse(int ni, const OpSpec& op) {
+    const PlanNode& n = pl.nodes[size_t(ni)];
+    int j_tail = -1;
+    for (size_t j = 0; j < n.sources.size(); ++j)
+      if (chain_tail.count(n.sources[j])) {
+        j_tail = int(j);
+        break;
+      }
+    if (j_tail < 0) return false;
+    const int src = n.sources[size_t(j_tail)];
+    const auto bp = chain_tail[src];
+    auto& spec = prog.gemm_specs[size_t(bp.first)][size_t(bp.second)];
+    if (spec.n_epi >= kMaxEpi) return false;
+    const int gstep = gemm_step[size_t(bp.first)];
+    EpiStage st;
+    switch (op.fn) {
+      case EwFn::pointwise_fn: st.op = EPI_TANH; break;
+      case EwFn::pointwise_fn_grad: st.op = EPI_DTANH; break;
+      case EwFn::scale: st.op = EPI_SCALE; st.scale = float(op.scale); break;
+      case EwFn::add: st.op = EPI_ADD; break;
+      case EwFn::sub: st.op = j_tail == 0 ? EPI_SUB_PO : EPI_SUB_OP; break;
+    }
+    if (n.sources.size() == 2) {
+      const int other = n.sources[size_t(1 - j_tail)];
+      if (other == src) return false;
+      if (pending[size_t(other)] >= 0) return false;  // produced by an open launch
+      const int avail = P.avail_step[size_t(other)];
+      if (gstep >= 0 && avail >= gstep) return false;
+      const StridedView& ov = value(other);
+      if (ov.rank != 2) return false;
+      st.other = ov.ptr;
+      st.o_rs = ov.st[0];
+      st.o_cs = ov.shape[1] == 1 ? 1 : ov.st[1];
+    }
+    const StridedView out = alloc(n.region.shape());
+    set_val(ni, out);
+    st.out = out.ptr;
+    st.out_rs = out.st[0];
+    st.out_cs = 1;
+    spec.epi[spec.n_epi++] = st;
+    chain_tail.erase(src);
+    chain_tail[ni] = bp;
+    P.n_fused++;
+    if (gstep >= 0) {
+      P.avail_step[size_t(ni)] = gstep;
+    } else {
+      produced(ni, C_COMPUTE);
+    }
+    return true;
+  }
+
+  // ------------------------------------------------------------ conversions
+  void copy_into(const StridedView& dst, const StridedView& src) {
+    o_copy.descs.push_back(nary_desc(NARY_COPY, dst, {src}));
+  }
+
+  void lower_fetch_or_slice(int ni) {
+    const PlanNode& n = pl.nodes[size_t(ni)];
+    const int src = n.sources[0];
+    const PlanNode& sn = pl.nodes[size_t(src)];
+    const bool dst_mine = mine_dev(n.device);
+    const bool src_mine = mine_dev(sn.device);
+    const bool remote = n.kind == NodeKind::fetch && (rank_of(n.device) != rank_of(sn.device) || force_xchg);
+    const int cat = defer_to[size_t(ni)];
+
+    if (n.kind == NodeKind::fetch && dst_mine) P.fetch_in += n.bytes;
+    if (!remote) {
+      if (!dst_mine) return;
+      if (n.kind == NodeKind::slice && cat < 0) {
+        set_val(ni, subview(value(src), sn.region, n.region));
+        P.avail_step[size_t(ni)] = P.avail_step[size_t(src)];
+        if (pending[size_t(src)] >= 0) produced(ni, Cls(pending[size_t(src)]));
+        return;
+      }
+      need(src, C_COPY);
+      const StridedView sv = subview(value(src), sn.region, n.region);
+      if (cat >= 0) {
+        ensure_alloc(cat);
+        const PlanNode& cn = pl.nodes[size_t(cat)];
+        copy_into(subview(P.val[size_t(cat)], cn.region, n.region), sv);
+      } else {
+        const StridedView d = alloc(n.region.shape());
+        set_val(ni, d);
+        copy_into(d, sv);
+        produced(ni, C_COPY);
+      }
+      return;
+    }
+    // cross-rank (or forced) transfer through NCCL
+    const size_t bytes = size_t(n.region.volume()) * 4;
+    if (src_mine) {
+      need(src, C_PACK);
+      const StridedView sv = subview(value(src), sn.region, n.region);
+      const float* sp = sv.ptr;
+      if (!sv.contiguous()) {
+        const StridedView st = alloc(n.region.shape());
+        o_pack.descs.push_back(nary_desc(NARY_COPY, st, {sv}));
+        sp = st.ptr;
+      }
+      o_xchg.x.push_back(Xfer{rank_of(n.device), true, const_cast<float*>(sp), bytes, ni});
+      o_xchg.bytes_out += int64_t(bytes);
+      if (rank_of(n.device) != C.rank) P.xrank_out += int64_t(bytes);
+    }
+    if (dst_mine) {
+      if (rank_of(sn.device) != C.rank) P.xrank_in += int64_t(bytes);
+      StridedView target;
+      bool direct = false;
+      if (cat >= 0) {
+        ensure_alloc(cat);
+        const PlanNode& cn = pl.nodes[size_t(cat)];
+        target = subview(P.val[size_t(cat)], cn.region, n.region);
+        direct = target.contiguous();
+      } else {
+        target = alloc(n.region.shape());
+        set_val(ni, target);
+        direct = true;
+      }
+      if (direct) {
+        o_xchg.x.push_back(Xfer{rank_of(sn.device), false, target.ptr, bytes, ni});
+        if (cat < 0) produced(ni, C_XCHG);
+      } else {
+        const StridedView stg = alloc(n.region.shape());
+        o_xchg.x.push_back(Xfer{rank_of(sn.device), false, stg.ptr, bytes, ni});
+        copy_into(target, stg);
+      }
+      o_xchg.bytes_in += int64_t(bytes);
+    }
+  }
+
+  void lower_concat(int ni) {
+    const PlanNode& n = pl.nodes[size_t(ni)];
+    if (!mine_dev(n.device)) return;
+    ensure_alloc(ni);
+    for (int s : n.sources) {
+      if (defer_to[size_t(s)] == ni) continue;  // already pasted by the piece itself
+      need(s, C_COPY);
+      const PlanNode& pn = pl.nodes[size_t(s)];
+      copy_into(subview(P.val[size_t(ni)], n.region, pn.region), value(s));
+    }
+    produced(ni, C_COPY);
+  }
+
+  void lower_reduce(int ni) {
+    const PlanNode& n = pl.nodes[size_t(ni)];
+    if (!mine_dev(n.device)) return;
+    std::vector<StridedView> ins;
+    for (int s : n.sources) {
+      need(s, C_REDUCE);
+      ins.push_back(value(s));
+    }
+    const StridedView out = alloc(n.region.shape());
+    set_val(ni, out);
+    // Sum in source order (execgraph.cpp:264-282 fixes that order).  More than 8 partials
+    // (k > 3) continue as out = out + next 7 in a following launch.
+    size_t i = std::min(ins.size(), size_t(kMaxIn));
+    o_reduce.descs.push_back(nary_desc(i == 1 ? NARY_COPY : NARY_SUM, out,
+                                       std::vector<StridedView>(ins.begin(), ins.begin() + long(i))));
+    while (i < ins.size()) {
+      produced(ni, C_REDUCE);
+      flush();
+      const size_t j = std::min(ins.size(), i + kMaxIn - 1);
+      std::vector<StridedView> chunk{out};
+      chunk.insert(chunk.end(), ins.begin() + long(i), ins.begin() + long(j));
+      o_reduce.descs.push_back(nary_desc(NARY_SUM, out, chunk));
+      i = j;
+    }
+    produced(ni, C_REDUCE);
+  }
+
+  void lower_buffer(int ni) {
+    const PlanNode& n = pl.nodes[size_t(ni)];
+    if (!mine_dev(n.device)) return;
+    const StridedView v = alloc(n.region.shape());
+    set_val(ni, v);
+    P.avail_step[size_t(ni)] = -1;
+    InitDesc d;
+    std::memset(&d, 0, sizeof d);
+    d.out = v.ptr;
+    const TensorSpec& t = pl.tensor(n.tensor);
+    const int r = int(t.shape.size());
+    if (r > kMaxRank) fail("tensor " + t.id + " has rank > 4");
+    d.rank = r;
+    const int pad = kMaxRank - r;
+    for (int i = 0; i < kMaxRank; ++i) {
+      if (i < pad) {
+        d.full[i] = 1;
+        d.lo[i] = 0;
+        d.ext[i] = 1;
+      } else {
+        d.full[i] = t.shape[size_t(i - pad)];
+        d.lo[i] = n.region.b[size_t(i - pad)][0];
+        d.ext[i] = n.region.b[size_t(i - pad)][1] - n.region.b[size_t(i - pad)][0];
+      }
+    }
+    d.n = n.region.volume();
+    d.state0 = fnv1a(t.id.data(), t.id.size());  // XORed with the seed at init time
+    P.init.descs.push_back(d);
+  }
+
+  void run_main() {
+    const size_t N = pl.nodes.size();
+    consumers.assign(N, 0);
+    defer_to.assign(N, -1);
+    is_holder.assign(N, 0);
+    pending.assign(N, -1);
+    for (const auto& kv : pl.holders)
+      for (int h : kv.second) is_holder[size_t(h)] = 1;
+    std::vector<int> last_consumer(N, -1);
+    for (size_t i = 0; i < N; ++i)
+      for (int s : pl.nodes[i].sources) {
+        consumers[size_t(s)]++;
+        last_consumer[size_t(s)] = int(i);
+      }
+    for (size_t i = 0; i < N; ++i) {
+      const PlanNode& n = pl.nodes[i];
+      if ((n.kind == NodeKind::fetch || n.kind == NodeKind::slice) && consumers[i] == 1 &&
+          !is_holder[i]) {
+        const int c = last_consumer[i];
+        if (pl.nodes[size_t(c)].kind == NodeKind::concat && pl.nodes[size_t(c)].device == n.device)
+          defer_to[i] = c;
+      }
+    }
+    std::string cur_phase;
+    bool seen_conv = false;
+    for (size_t i = 0; i < N; ++i) {
+      const PlanNode& n = pl.nodes[i];
+      if (n.phase != cur_phase) {
+        flush();
+        cur_phase = n.phase;
+        seg_op = op_of_phase(n.phase);
+        seen_conv = false;
+      }
+      switch (n.kind) {
+        case NodeKind::buffer: lower_buffer(int(i)); break;
+        case NodeKind::sub_op:
+          if (seen_conv) flush();  // a compute after conversions starts a new segment
+          if (mine_dev(n.device)) lower_sub_op(int(i));
+          break;
+        case NodeKind::slice:
+        case NodeKind::fetch: seen_conv = true; lower_fetch_or_slice(int(i)); break;
+        case NodeKind::concat: seen_conv = true; lower_concat(int(i)); break;
+        case NodeKind::reduce_partial: seen_conv = true; lower_reduce(int(i)); break;
+      }
+    }
+    flush();
+  }
+
+  // Loop carry: every "<w>_next" holder block onto the holder blocks of weight "<w>".
+  void run_carry() {
+    for (const auto& kv : pl.tensors) {
+      const std::string& id = kv.first;
+      if (id.size() <= 5 || id.compare(id.size() - 5, 5, "_next") != 0) continue;
+      const std::string base = id.substr(0, id.size() - 5);
+      if (!pl.tensors.count(base)) continue;
+      if (pl.tensors.at(base).shape != kv.second.shape) continue;
+      const auto& src_h = pl.holders.at(id);
+      const auto& dst_h = pl.holders.at(base);
+      for (int d = 0; d < pl.devices; ++d) {
+        const int dn = dst_h[size_t(d)];
+        const PlanNode& dnode = pl.nodes[size_t(dn)];
+        if (dnode.kind != NodeKind::buffer)
+          fail("loop carry: weight " + base + " is not a graph input on device " + std::to_string(d));
+        // pieces: local overlap first, then the lowest-numbered holder of each region cell,
+        // preferring holders on the destination's own rank
+        std::vector<std::pair<Region, int>> pieces;
+        std::vector<Region> remaining{dnode.region};
+        auto take = [&](int e) {
+          const Region& have = pl.nodes[size_t(src_h[size_t(e)])].region;
+          std::vector<Region> next;
+          for (const auto& box : remaining) {
+            const Region ov = box.intersect(have);
+            if (ov.volume() == 0) {
+              next.push_back(box);
+              continue;
+            }
+            pieces.push_back({ov, e});
+            // peel the remainder of box minus ov into disjoint boxes
+            Region rest = box;
+            for (int dd = 0; dd < rest.rank(); ++dd) {
+              if (rest.b[size_t(dd)][0] < ov.b[size_t(dd)][0]) {
+                Region lo = rest;
+                lo.b[size_t(dd)][1] = ov.b[size_t(dd)][0];
+                next.push_back(lo);
+                rest.b[size_t(dd)][0] = ov.b[size_t(dd)][0];
+              }
+              if (rest.b[size_t(dd)][1] > ov.b[size_t(dd)][1]) {
+                Region hi = rest;
+                hi.b[size_t(dd)][0] = ov.b[size_t(dd)][1];
+                next.push_back(hi);
+                rest.b[size_t(dd)][1] = ov.b[size_t(dd)][1];
+              }
+            }
+          }
+          remaining.swap(next);
+        };
+        take(d);
+        for (int e = 0; e < pl.devices && !remaining.empty(); ++e)
+          if (e != d && rank_of(e) == rank_of(d)) take(e);
+        for (int e = 0; e < pl.devices && !remaining.empty(); ++e)
+          if (rank_of(e) != rank_of(d)) take(e);
+        if (!remaining.empty()) fail("loop carry: no holder covers part of " + id);
+        for (const auto& pc : pieces) {
+          const int e = pc.second;
+          const int sn = src_h[size_t(e)];
+          const PlanNode& snode = pl.nodes[size_t(sn)];
+          const size_t bytes = size_t(pc.first.volume()) * 4;
+          const bool remote = rank_of(e) != rank_of(d) || (force_xchg && e != d);
+          if (e != d) P.carry_bytes += int64_t(bytes);
+          if (!remote) {
+            if (!mine_dev(d)) continue;
+            copy_into(subview(P.val[size_t(dn)], dnode.region, pc.first),
+                      subview(value(sn), snode.region, pc.first));
+            continue;
+          }
+          if (mine_dev(e)) {
+            const StridedView sv = subview(value(sn), snode.region, pc.first);
+            const float* sp = sv.ptr;
+            if (!sv.contiguous()) {
+              const StridedView st = alloc(pc.first.shape());
+              o_pack.descs.push_back(nary_desc(NARY_COPY, st, {sv}));
+              sp = st.ptr;
+            }
+            o_xchg.x.push_back(Xfer{rank_of(d), true, const_cast<float*>(sp), bytes, sn});
+            if (rank_of(d) != C.rank) P.carry_xrank += int64_t(bytes);
+          }
+          if (mine_dev(d)) {
+            const StridedView target = subview(P.val[size_t(dn)], dnode.region, pc.first);
+            if (target.contiguous()) {
+              o_xchg.x.push_back(Xfer{rank_of(e), false, target.ptr, bytes, dn});
+            } else {
+              const StridedView stg = alloc(pc.first.shape());
+              o_xchg.x.push_back(Xfer{rank_of(e), false, stg.ptr, bytes, dn});
+              copy_into(target, stg);
+            }
+          }
+        }
+      }
+    }
+    seg_op = "carry";
+    flush();
+  }
+};
+
+void lower(PlanRt& P, bool dry) {
+  P.main = Program{};
+  P.carry = Program{};
+  P.init = InitBatch{};
+  P.val.assign(P.plan.nodes.size(), StridedView{});
+  P.has_val.assign(P.plan.nodes.size(), 0);
+  P.avail_step.assign(P.plan.nodes.size(), -1);
+  P.arena_used = 0;
+  P.fetch_in = P.xrank_in = P.xrank_out = P.carry_bytes = P.carry_xrank = 0;
+  P.n_fused = 0;
+  P.gemm_flops = P.gemm_min_bytes = 0;
+  if (dry) P.base = kFakeBase;
+  {
+    Lowerer L(P, P.main, dry);
+    L.run_main();
+  }
+  {
+    Lowerer L(P, P.carry, dry);
+    L.pending.assign(P.plan.nodes.size(), -1);
+    L.run_carry();
+  }
+}
+
+void prepare_program(PlanRt& P, Program& prog) {
+  for (auto& b : prog.nary) nary_prepare(b);
+  for (auto& b : prog.conv) conv_prepare(b);
+  for (auto& specs : prog.gemm_specs)
+    prog.gemm.push_back(gemm_prepare(specs, P.ctx->num_sms, P.precision == 1));
+}
+
+void free_program(Program& prog) {
+  for (auto& b : prog.nary) nary_free(b);
+  for (auto& b : prog.conv) conv_free(b);
+  for (auto& g : prog.gemm) gemm_free(g);
+  prog = Program{};
+}
+
+}  // namespace
+
+PlanRt::~PlanRt() {
+  free_program(main);
+  free_program(carry);
+  init_free(init);
+  for (auto e : events) cudaEventDestroy(e);
+  if (io_tmp) cudaFree(io_tmp);
+  if (arena) cudaFree(arena);
+}
+
+PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
+  auto P = std::make_unique<PlanRt>();
+  P->ctx = ctx;
+  P->plan = parse_plan(json);
+  P->precision = precision;
+  P->flags = flags;
+  P->stream = ctx->stream;
+  if (precision != 0 && precision != 1) fail("unknown precision " + std::to_string(precision));
+  for (const auto& kv : P->plan.tensors)
+    if (kv.second.dtype_bytes != 4)
+      fail("tensor " + kv.first + " has dtype_bytes " + std::to_string(kv.second.dtype_bytes) +
+           "; this executor runs fp32 (dtype_bytes 4) plans");
+  const int devices = P->plan.devices;
+  if (ctx->world > devices)
+    fail("plan has " + std::to_string(devices) + " devices but the job has " + std::to_string(ctx->world) + " ranks");
+  if (devices % ctx->world != 0) fail("plan devices must be a multiple of the rank count");
+  P->dev_rank.resize(size_t(devices));
+  for (int d = 0; d < devices; ++d) P->dev_rank[size_t(d)] = int((int64_t(d) * ctx->world) / devices);
+  lower(*P, true);
+  if (!ctx->host_only()) {
+    if ((flags & 2) || ctx->world > 1) {
+      if (!ctx->comm) {
+        if (ctx->world > 1) fail("multi-rank plan needs tpx_init_comm first");
+        char uid[128];
+        nccl_unique_id(uid);
+        ctx->comm = nccl_comm_init(1, uid, 0);
+      }
+    }
+    P->arena_bytes = std::max<size_t>(P->arena_used, kAlign);
+    CUDA_CHECK(cudaMalloc(&P->arena, P->arena_bytes));
+    P->base = reinterpret_cast<uintptr_t>(P->arena);
+    lower(*P, false);
+    prepare_program(*P, P->main);
+    prepare_program(*P, P->carry);
+    init_prepare(P->init);
+  } else {
+    P->arena_bytes = P->arena_used;
+  }
+  return P.release();
+}
+
+static void launch_step(PlanRt& P, Program& prog, const Step& s, cudaStream_t st) {
+  switch (s.kind) {
+    case ST_NARY: nary_run(prog.nary[size_t(s.idx)], st); break;
+    case ST_GEMM: gemm_run(prog.gemm[size_t(s.idx)], st); break;
+    case ST_CONV: conv_run(prog.conv[size_t(s.idx)], st); break;
+    case ST_XCHG: {
+      const XchgGroup& g = prog.xchg[size_t(s.idx)];
+      nccl_group_start();
+      for (const auto& x : g.x) {
+        if (x.send) nccl_send(x.ptr, x.bytes, x.peer, P.ctx->comm, st);
+        else nccl_recv(x.ptr, x.bytes, x.peer, P.ctx->comm, st);
+      }
+      nccl_group_end();
+      break;
+    }
+  }
+}
+
+void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
+  if (P.ctx->host_only()) fail("host-only context cannot execute plans");
+  cudaStream_t st = P.stream;
+  if (!P.timing || only_op) {
+    for (const auto& s : prog.steps)
+      if (!only_op || s.op == *only_op) launch_step(P, prog, s, st);
+    return;
+  }
+  const size_t n = prog.steps.size();
+  while (P.events.size() < n + 1) {
+    cudaEvent_t e;
+    CUDA_CHECK(cudaEventCreate(&e));
+    P.events.push_back(e);
+  }
+  CUDA_CHECK(cudaEventRecord(P.events[0], st));
+  for (size_t i = 0; i < n; ++i) {
+    launch_step(P, prog, prog.steps[i], st);
+    CUDA_CHECK(cudaEventRecord(P.events[i + 1], st));
+  }
+  CUDA_CHECK(cudaEventSynchronize(P.events[n]));
+  P.last_total_ms = P.last_gemm_ms = P.last_copy_ms = 0;
+  for (size_t i = 0; i < n; ++i) {
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, P.events[i], P.events[i + 1]));
+    P.last_total_ms += ms;
+    if (prog.steps[i].kind == ST_GEMM) P.last_gemm_ms += ms;
+    else if (prog.steps[i].kind == ST_NARY || prog.steps[i].kind == ST_XCHG) P.last_copy_ms += ms;
+  }
+}
+
+void init_inputs(PlanRt& P, uint64_t seed) {
+  if (P.ctx->host_only()) fail("host-only context cannot execute plans");
+  if (P.init.descs.empty()) return;
+  // re-key the descriptors with the seed (state0 = seed ^ fnv1a(id), dense.cpp:51)
+  std::vector<uint64_t> keys;
+  for (auto& d : P.init.descs) keys.push_back(d.state0);
+  for (auto& d : P.init.descs) d.state0 ^= seed;
+  init_prepare(P.init);
+  for (size_t i = 0; i < keys.size(); ++i) P.init.descs[i].state0 = keys[i];
+  init_run(P.init, P.stream);
+}
+
+static void ensure_io(PlanRt& P, int64_t n) {
+  if (P.io_tmp_elems >= size_t(n)) return;
+  if (P.io_tmp) cudaFree(P.io_tmp);
+  CUDA_CHECK(cudaMalloc(&P.io_tmp, size_t(std::max<int64_t>(n, 1)) * 4));
+  P.io_tmp_elems = size_t(n);
+}
+
+static const StridedView& node_val(PlanRt& P, int node, int64_t n) {
+  if (P.ctx->host_only()) fail("host-only context holds no values");
+  if (!P.has_val[size_t(node)])
+    fail("node " + P.plan.nodes[size_t(node)].id + " has no value on this rank");
+  const StridedView& v = P.val[size_t(node)];
+  if (v.elements() != n)
+    fail("buffer has " + std::to_string(n) + " elements, node " + P.plan.nodes[size_t(node)].id +
+         " holds " + std::to_string(v.elements()));
+  return v;
+}
+
+void read_node_f32(PlanRt& P, int node, float* dst, int64_t n) {
+  const StridedView& v = node_val(P, node, n);
+  const float* src = v.ptr;
+  if (!v.contiguous()) {
+    ensure_io(P, n);
+    NaryBatch b;
+    b.descs.push_back(nary_desc(NARY_COPY, contiguous_view(P.io_tmp, std::vector<int64_t>(v.shape, v.shape + v.rank)), {v}));
+    nary_prepare(b);
+    nary_run(b, P.stream);
+    CUDA_CHECK(cudaStreamSynchronize(P.stream));
+    nary_free(b);
+    src = P.io_tmp;
+  }
+  CUDA_CHECK(cudaMemcpyAsync(dst, src, size_t(n) * 4, cudaMemcpyDeviceToHost, P.stream));
+  CUDA_CHECK(cudaStreamSynchronize(P.stream));
+}
+
+void write_node_f32(PlanRt& P, int node, const float* src, int64_t n) {
+  const StridedView& v = node_val(P, node, n);
+  if (v.contiguous()) {
+    CUDA_CHECK(cudaMemcpyAsync(v.ptr, src, size_t(n) * 4, cudaMemcpyHostToDevice, P.stream));
+    return;
+  }
+  ensure_io(P, n);
+  CUDA_CHECK(cudaMemcpyAsync(P.io_tmp, src, size_t(n) * 4, cudaMemcpyHostToDevice, P.stream));
+  NaryBatch b;
+  b.descs.push_back(nary_desc(NARY_COPY, v, {contiguous_view(P.io_tmp, std::vector<int64_t>(v.shape, v.shape + v.rank))}));
+  nary_prepare(b);
+  nary_run(b, P.stream);
+  CUDA_CHECK(cudaStreamSynchronize(P.stream));
+  nary_free(b);
+}
+
+void read_node(PlanRt& P, int node, double* dst, int64_t n) {
+  std::vector<float> tmp(size_t(std::max<int64_t>(n, 1)));
+  read_node_f32(P, node, tmp.data(), n);
+  f32_to_f64_host(tmp.data(), dst, n);
+}
+
+void write_node(PlanRt& P, int node, const double* src, int64_t n) {
+  std::vector<float> tmp(size_t(std::max<int64_t>(n, 1)));
+  for (int64_t i = 0; i < n; ++i) tmp[size_t(i)] = float(src[i]);
+  write_node_f32(P, node, tmp.data(), n);
+  CUDA_CHECK(cudaStreamSynchronize(P.stream));
+}
+
+std::string describe(const PlanRt& P) {
+  std::ostringstream o;
+  auto prog_json = [&](const Program& prog) {
+    std::ostringstream s;
+    s << "{\"steps\":[";
+    for (size_t i = 0; i < prog.steps.size(); ++i) {
+      const Step& st = prog.steps[i];
+      if (i) s << ",";
+      s << "{\"kind\":" << json_quote(st.kind == ST_NARY ? "nary" : st.kind == ST_GEMM ? "gemm" : st.kind == ST_CONV ? "conv" : "nccl")
+        << ",\"op\":" << json_quote(st.op) << ",\"what\":" << json_quote(st.what);
+      if (st.kind == ST_NARY) {
+        const NaryBatch& b = prog.nary[size_t(st.idx)];
+        s << ",\"descs\":" << b.descs.size();
+        double bytes = 0;
+        for (const auto& d : b.descs) bytes += 4.0 * double(d.units) * d.vec * (d.nin + 1);
+        s << ",\"bytes\":" << int64_t(bytes);
+      } else if (st.kind == ST_GEMM) {
+        const auto& specs = prog.gemm_specs[size_t(st.idx)];
+        s << ",\"problems\":" << specs.size() << ",\"shapes\":[";
+        for (size_t j = 0; j < specs.size(); ++j) {
+          const GemmSpec& g = specs[j];
+          const long long M = g.ta ? g.a.cols : g.a.rows, K = g.ta ? g.a.rows : g.a.cols;
+          const long long N = g.tb ? g.b.rows : g.b.cols;
+          if (j) s << ",";
+          s << "[" << M << "," << N << "," << K << "," << g.n_epi << "]";
+        }
+        s << "],\"ta\":" << (specs.empty() ? 0 : specs[0].ta) << ",\"tb\":" << (specs.empty() ? 0 : specs[0].tb);
+        if (size_t(st.idx) < prog.gemm.size()) {
+          const GemmLaunch& gl = prog.gemm[size_t(st.idx)];
+          s << ",\"bn\":" << gl.bn << ",\"swap\":" << gl.swap << ",\"units\":" << gl.units
+            << ",\"splits\":" << (gl.host_problems.empty() ? 1 : gl.host_problems[0].splits);
+        }
+      } else if (st.kind == ST_XCHG) {
+        const XchgGroup& g = prog.xchg[size_t(st.idx)];
+        s << ",\"xfers\":[";
+        for (size_t j = 0; j < g.x.size(); ++j) {
+          const Xfer& x = g.x[j];
+          if (j) s << ",";
+          s << "{\"peer\":" << x.peer << ",\"send\":" << (x.send ? 1 : 0) << ",\"bytes\":" << x.bytes
+            << ",\"node\":" << json_quote(P.plan.nodes[size_t(x.node)].id) << "}";
+        }
+        s << "],\"bytes_in\":" << g.bytes_in << ",\"bytes_out\":" << g.bytes_out;
+      } else if (st.kind == ST_CONV) {
+        s << ",\"descs\":" << prog.conv[size_t(st.idx)].descs.size();
+      }
+      s << "}";
+    }
+    s << "]}";
+    return s.str();
+  };
+  o << "{\"rank\":" << P.ctx->rank << ",\"world\":" << P.ctx->world << ",\"k\":" << P.plan.k
+    << ",\"devices\":" << P.plan.devices << ",\"device_rank\":[";
+  for (size_t d = 0; d < P.dev_rank.size(); ++d) o << (d ? "," : "") << P.dev_rank[d];
+  o << "],\"fetch_bytes_total\":" << P.plan.fetch_bytes_total << ",\"rank_fetch_bytes_in\":" << P.fetch_in
+    << ",\"rank_xrank_bytes_in\":" << P.xrank_in << ",\"rank_xrank_bytes_out\":" << P.xrank_out
+    << ",\"carry_bytes\":" << P.carry_bytes << ",\"carry_xrank_bytes_out\":" << P.carry_xrank
+    << ",\"fused_elementwise\":" << P.n_fused << ",\"arena_bytes\":" << P.arena_used
+    << ",\"gemm_flops\":" << P.gemm_flops << ",\"main\":" << prog_json(P.main)
+    << ",\"carry\":" << prog_json(P.carry) << "}";
+  return o.str();
+}
+
+}  // namespace tpx

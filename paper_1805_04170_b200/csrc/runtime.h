@@ -1,0 +1,111 @@
+// Plan lowering and execution: the B200 replacement for execute_numeric's node interpreter
+// (proj/src/simulator.cpp:55-127).
+//
+// Lowering turns the per-device node list into a short program of batched launches for the
+// logical devices this rank owns, phase by phase (phases as defined by
+// ExecutionPlan::phase_order, execgraph.cpp:41-47):
+//   sub_op nodes of the phase's op -> one grouped tcgen05 GEMM / conv / elementwise launch
+//                                     (elementwise consumers folded into GEMM epilogues)
+//   slice                           -> zero-copy strided view (or a copy straight into the
+//                                     concat that consumes it)
+//   fetch (same rank)               -> HBM copy (into the consuming concat when there is one)
+//   fetch (other rank)              -> pack (if strided) + NCCL send/recv group + unpack
+//   concat                          -> one buffer; every piece lands at its offset
+//   reduce_partial                  -> ordered sum of the partials (deterministic)
+// Every node value is an immutable strided fp32 view into one HBM arena.
+#pragma once
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "gemm.h"
+#include "kernels.h"
+#include "plan.h"
+
+namespace tpx {
+
+struct Ctx {
+  int ordinal = -1;   // CUDA device, -1 = host-only (lowering / accounting, no execution)
+  int rank = 0, world = 1;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  void* comm = nullptr;  // NCCL communicator (world > 1 or forced exchange)
+  bool host_only() const { return ordinal < 0; }
+};
+
+enum StepKind { ST_NARY, ST_GEMM, ST_CONV, ST_XCHG };
+
+struct Step {
+  StepKind kind;
+  int idx;             // into the batch vector of that kind
+  std::string op;      // owning op id (phase prefix)
+  std::string what;    // "pack" / "copy" / "reduce" / "ew" / "materialize" / "gemm" ...
+};
+
+struct Xfer {
+  int peer;
+  bool send;
+  void* ptr;
+  size_t bytes;
+  int node;            // fetch node index
+};
+
+struct XchgGroup {
+  std::vector<Xfer> x;
+  int64_t bytes_in = 0, bytes_out = 0;
+};
+
+struct Program {
+  std::vector<Step> steps;
+  std::vector<NaryBatch> nary;
+  std::vector<std::vector<GemmSpec>> gemm_specs;
+  std::vector<GemmLaunch> gemm;
+  std::vector<ConvBatch> conv;
+  std::vector<XchgGroup> xchg;
+};
+
+struct PlanRt {
+  Ctx* ctx = nullptr;
+  Plan plan;
+  int precision = 0;
+  int flags = 0;
+  std::vector<int> dev_rank;
+  std::vector<StridedView> val;
+  std::vector<char> has_val;
+  std::vector<int> avail_step;   // first step index after which the value exists
+  // arena
+  char* arena = nullptr;
+  size_t arena_bytes = 0, arena_used = 0;
+  uintptr_t base = 0;
+  // programs
+  Program main, carry;
+  InitBatch init;
+  // accounting
+  int64_t fetch_in = 0, xrank_in = 0, xrank_out = 0, carry_bytes = 0, carry_xrank = 0;
+  int n_fused = 0;
+  double gemm_flops = 0, gemm_min_bytes = 0;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> events;
+  double last_total_ms = 0, last_gemm_ms = 0, last_copy_ms = 0;
+  float* io_tmp = nullptr;
+  size_t io_tmp_elems = 0;
+  cudaStream_t stream = nullptr;
+
+  ~PlanRt();
+  bool mine(int node) const { return dev_rank[size_t(plan.nodes[size_t(node)].device)] == ctx->rank; }
+};
+
+PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags);
+void run_program(PlanRt& p, Program& prog, const std::string* only_op);
+void init_inputs(PlanRt& p, uint64_t seed);
+void read_node(PlanRt& p, int node, double* dst, int64_t n);
+void write_node(PlanRt& p, int node, const double* src, int64_t n);
+void read_node_f32(PlanRt& p, int node, float* dst, int64_t n);
+void write_node_f32(PlanRt& p, int node, const float* src, int64_t n);
+std::string describe(const PlanRt& p);
+
+}  // namespace tpx

@@ -61,7 +61,9 @@ _SIGS = {
     "tpx_last_timing": [c_vp, P(c_dbl), P(c_dbl), P(c_dbl)],
     "tpx_enable_timing": [c_vp, c_int],
     "tpx_gemm": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_i64,
-                 c_int, P(c_int), P(ctypes.c_float), P(c_vp), P(c_i64), P(c_vp), P(c_i64), c_u64],
+                 c_int, P(c_int), P(ctypes.c_float), P(c_vp), P(c_i64), P(c_vp), P(c_i64), c_int,
+                 c_u64],
+    "tpx_debug_gemm_mn_desc": [ctypes.c_uint, ctypes.c_uint],
 }
 
 
@@ -99,7 +101,7 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None):
+def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None, precision: int = 0):
     """C = op(A) @ op(B) on the tcgen05 path; A, B, C are 2-D fp32 CUDA tensors with unit
     inner stride.  `epi` = [(op, scale, other_or_None, out), ...] (gemm.h EpiOp codes)."""
     import torch  # plumbing only: device pointers and the current stream
@@ -118,4 +120,4 @@ def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None):
     s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
     check(lib().tpx_gemm(_ptr(A), A.shape[0], A.shape[1], A.stride(0), _ptr(B), B.shape[0],
                          B.shape[1], B.stride(0), int(ta), int(tb), _ptr(C), C.stride(0), n, ops,
-                         scales, others, others_rs, outs, outs_rs, s))
+                         scales, others, others_rs, outs, outs_rs, int(precision), s))

@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 from paper_1805_04170_b200 import native  # noqa: E402
 
 
-def run(M, N, K, ta, tb, epi=None, pad=0):
+def run(M, N, K, ta, tb, epi=None, pad=0, precision=0):
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(M * 7 + N * 3 + K)
     A = torch.rand((K, M) if ta else (M, K), device=dev, generator=g) * 2 - 1
@@ -29,7 +29,8 @@ def run(M, N, K, ta, tb, epi=None, pad=0):
         for op in epi:
             outs.append(torch.full((M, N), float("nan"), device=dev))
     W = torch.rand((M, N), device=dev, generator=g) * 2 - 1
-    native.gemm(A, B, ta, tb, C, epi=[(op, 0.01, W if op >= 4 else None, o) for op, o in zip(epi or [], outs)])
+    native.gemm(A, B, ta, tb, C, epi=[(op, 0.01, W if op >= 4 else None, o) for op, o in zip(epi or [], outs)],
+                precision=precision)
     torch.cuda.synchronize()
     ref = (A.double().T if ta else A.double()) @ (B.double().T if tb else B.double())
     err = ((C.double() - ref).abs().max() / ref.abs().max()).item()
@@ -50,17 +51,17 @@ def run(M, N, K, ta, tb, epi=None, pad=0):
     return res
 
 
-def bench(M, N, K, ta, tb, iters=20):
+def bench(M, N, K, ta, tb, iters=20, precision=0):
     A = torch.rand((K, M) if ta else (M, K), device="cuda")
     B = torch.rand((N, K) if tb else (K, N), device="cuda")
     C = torch.empty((M, N), device="cuda")
     for _ in range(3):
-        native.gemm(A, B, ta, tb, C)
+        native.gemm(A, B, ta, tb, C, precision=precision)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(iters):
-        native.gemm(A, B, ta, tb, C)
+        native.gemm(A, B, ta, tb, C, precision=precision)
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / iters
@@ -113,6 +114,16 @@ def main():
         print(f"{'ok ' if good else 'BAD'} epilogue {epi} err={errs}")
     errs = run(32, 512, 512, False, False, epi=[3, 6])
     print(f"{'ok ' if all(e <= 2e-3 for e in errs) else 'BAD'} swapped epilogue err={errs}")
+    # 3xTF32: fp32-accurate products
+    for c in cases:
+        errs = run(*c, precision=1)
+        good = all(e <= 5e-6 for e in errs)
+        ok &= good
+        print(f"{'ok ' if good else 'BAD'} 3xTF32 M,N,K,ta,tb={c} err={errs}")
+    errs = run(512, 512, 256, False, False, epi=[1, 2], precision=1)
+    good = all(e <= 5e-6 for e in errs)
+    ok &= good
+    print(f"{'ok ' if good else 'BAD'} 3xTF32 epilogue [1,2] err={errs}")
     if "--bench" in sys.argv:
         for c in [(512, 8192, 8192, False, False), (512, 8192, 8192, False, True),
                   (8192, 8192, 512, True, False), (64, 8192, 8192, False, False),
