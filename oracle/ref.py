@@ -72,6 +72,11 @@ def lib():
         L.ref_session_times.argtypes = [ctypes.c_void_p, P(c_dbl), P(c_dbl)]
         L.ref_session_serial.argtypes = [ctypes.c_void_p, c_char_p, P(c_dbl), c_i64]
         L.ref_session_node.argtypes = [ctypes.c_void_p, c_char_p, P(c_dbl), c_i64]
+        L.ref_pool_new.argtypes = [c_char_p, c_u64, c_int]
+        L.ref_pool_new.restype = ctypes.c_void_p
+        L.ref_pool_step.argtypes = [ctypes.c_void_p, P(c_dbl)]
+        L.ref_pool_step.restype = c_int
+        L.ref_pool_free.argtypes = [ctypes.c_void_p]
         for f in (L.ref_execute_numeric, L.ref_execute_numeric_parallel, L.ref_serial_seconds,
                   L.ref_session_times, L.ref_session_serial, L.ref_session_node):
             f.restype = c_int
@@ -197,3 +202,28 @@ class Session:
                 ctypes.POINTER(ctypes.c_double)), out.size):
             raise RefError(lib().ref_last_error().decode())
         return out
+
+
+class Pool:
+    """`threads` independent copies of the reference's tiled node loop on the same plan;
+    step() runs all copies concurrently (one per host thread) and returns the wall time."""
+
+    def __init__(self, plan_json: str, seed: int, threads: int):
+        self.threads = threads
+        self._h = lib().ref_pool_new(_b(plan_json), seed, threads)
+        if not self._h:
+            raise RefError(lib().ref_last_error().decode())
+
+    def step(self) -> float:
+        s = ctypes.c_double()
+        if lib().ref_pool_step(self._h, ctypes.byref(s)):
+            raise RefError(lib().ref_last_error().decode())
+        return s.value
+
+    def close(self):
+        if self._h:
+            lib().ref_pool_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

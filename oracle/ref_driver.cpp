@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -383,5 +384,68 @@ int ref_session_serial(void* h, const char* tensor, double* out, std::int64_t n)
 int ref_session_node(void* h, const char* node_id, double* out, std::int64_t n) {
   return guard_int([&] { copy_out(static_cast<Session*>(h)->values.at(node_id).dense, out, n); });
 }
+
+// A pool of `threads` sessions of the same plan (the reference is single-threaded; the CPU
+// baseline uses every host core by running independent copies).  ref_pool_step re-runs the
+// reference's tiled node loop (execute_numeric's simulator.cpp:77-127 semantics through the
+// reference's extract_region / paste_region / run_op_dense) on every copy concurrently and
+// returns the wall time.
+struct Pool {
+  std::vector<std::unique_ptr<Session>> s;
+};
+
+void* ref_pool_new(const char* plan_json, std::uint64_t seed, int threads) {
+  try {
+    auto* p = new Pool;
+    ExecutionPlan plan = parse_plan(plan_json);
+    p->s.resize(static_cast<std::size_t>(threads));
+    std::vector<std::thread> pool;
+    std::vector<std::string> errs(static_cast<std::size_t>(threads));
+    for (int i = 0; i < threads; ++i)
+      pool.emplace_back([&, i] {
+        try {
+          auto s = std::make_unique<Session>();
+          s->plan = plan;
+          s->serial = serial_execute(s->plan.graph, seed);
+          p->s[static_cast<std::size_t>(i)] = std::move(s);
+        } catch (const std::exception& e) {
+          errs[static_cast<std::size_t>(i)] = e.what();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (!e.empty()) {
+        delete p;
+        fail(e);
+      }
+    return p;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+int ref_pool_step(void* h, double* seconds) {
+  return guard_int([&] {
+    auto* p = static_cast<Pool*>(h);
+    std::vector<std::thread> pool;
+    std::vector<std::string> errs(p->s.size());
+    auto t0 = std::chrono::steady_clock::now();
+    for (std::size_t i = 0; i < p->s.size(); ++i)
+      pool.emplace_back([&, i] {
+        try {
+          run_nodes(*p->s[i], FunctionBindings::standard());
+        } catch (const std::exception& e) {
+          errs[i] = e.what();
+        }
+      });
+    for (auto& t : pool) t.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (auto& e : errs)
+      if (!e.empty()) fail(e);
+  });
+}
+
+void ref_pool_free(void* h) { delete static_cast<Pool*>(h); }
 
 }  // extern "C"

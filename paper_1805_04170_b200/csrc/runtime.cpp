@@ -333,7 +333,11 @@ struct Lowerer {
     const bool remote = n.kind == NodeKind::fetch && (rank_of(n.device) != rank_of(sn.device) || force_xchg);
     const int cat = defer_to[size_t(ni)];
 
-    if (n.kind == NodeKind::fetch && dst_mine) P.fetch_in += n.bytes;
+    if (n.kind == NodeKind::fetch && dst_mine) {
+      P.fetch_in += n.bytes;
+      P.op_bytes_in[op_of_phase(n.phase)] += n.bytes;
+      P.phase_bytes_in[n.phase] += n.bytes;
+    }
     if (!remote) {
       if (!dst_mine) return;
       if (n.kind == NodeKind::slice && cat < 0) {
@@ -621,6 +625,9 @@ void lower(PlanRt& P, bool dry) {
   P.arena_used = 0;
   P.fetch_in = P.xrank_in = P.xrank_out = P.carry_bytes = P.carry_xrank = 0;
   P.n_fused = 0;
+  P.op_bytes_in.clear();
+  P.phase_bytes_in.clear();
+  for (const auto& op : P.plan.ops) P.op_bytes_in[op.id] = 0;
   P.gemm_flops = P.gemm_min_bytes = 0;
   if (dry) P.base = kFakeBase;
   {
@@ -881,7 +888,20 @@ std::string describe(const PlanRt& P) {
     << ",\"rank_xrank_bytes_in\":" << P.xrank_in << ",\"rank_xrank_bytes_out\":" << P.xrank_out
     << ",\"carry_bytes\":" << P.carry_bytes << ",\"carry_xrank_bytes_out\":" << P.carry_xrank
     << ",\"fused_elementwise\":" << P.n_fused << ",\"arena_bytes\":" << P.arena_used
-    << ",\"gemm_flops\":" << P.gemm_flops << ",\"main\":" << prog_json(P.main)
+    << ",\"gemm_flops\":" << P.gemm_flops;
+  auto map_json = [&](const std::map<std::string, int64_t>& m) {
+    std::ostringstream s;
+    s << "{";
+    bool first = true;
+    for (const auto& kv : m) {
+      s << (first ? "" : ",") << json_quote(kv.first) << ":" << kv.second;
+      first = false;
+    }
+    s << "}";
+    return s.str();
+  };
+  o << ",\"per_op_fetch_bytes_in\":" << map_json(P.op_bytes_in)
+    << ",\"per_phase_fetch_bytes_in\":" << map_json(P.phase_bytes_in) << ",\"main\":" << prog_json(P.main)
     << ",\"carry\":" << prog_json(P.carry) << "}";
   return o.str();
 }

@@ -86,6 +86,7 @@ struct PlanRt {
   // accounting
   int64_t fetch_in = 0, xrank_in = 0, xrank_out = 0, carry_bytes = 0, carry_xrank = 0;
   int n_fused = 0;
+  std::map<std::string, int64_t> op_bytes_in, phase_bytes_in;  // fetch bytes landing on this rank
   double gemm_flops = 0, gemm_min_bytes = 0;
   // timing
   bool timing = false;

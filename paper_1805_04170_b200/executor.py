@@ -86,11 +86,11 @@ class PlanExecutor:
                  flags: int = FLAG_FUSE):
         self.ctx = ctx
         self.plan_text = plan_json if isinstance(plan_json, str) else plan_json.decode()
-        self.plan = json.loads(self.plan_text)
         raw = self.plan_text.encode()
         h = ctypes.c_void_p()
         check(lib().tpx_load_plan(ctx._h, raw, len(raw), precision, flags, ctypes.byref(h)))
         self._h = h
+        self.plan = json.loads(self.plan_text)
         self._nodes = {n["id"]: n for n in self.plan["nodes"]}
 
     # ---------------------------------------------------------------- lifecycle
@@ -134,6 +134,8 @@ class PlanExecutor:
 
     # ---------------------------------------------------------------- node values
     def node_shape(self, node_id: str):
+        if node_id not in self._nodes:
+            raise TpxError(f"unknown node '{node_id}'")
         return [hi - lo for lo, hi in self._nodes[node_id]["region"]]
 
     def read_node(self, node_id: str) -> np.ndarray:

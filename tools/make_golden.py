@@ -1,21 +1,26 @@
-"""Generate tests/golden/ fixtures from the COMPILED REFERENCE (oracle/_ref).
+"""Generates tests/golden/ from the UNMODIFIED reference (oracle/_ref, built by oracle/Makefile
+from /root/reference/proj/src).  Test infrastructure only; runs in the build container.
 
-Run in the build container (needs /root/reference to build oracle/_ref):
-    python tools/make_golden.py
+For every case: the graph comes from the reference's own generators (gen_mlp / gen_cnn,
+proj/src/graph.cpp:179-314) or, for the reduce KAT, the graph of
+proj/tests/test_plan.cpp:191-223; the assignment from preset_assignment / kcuts
+(proj/src/assign.cpp:36-81, proj/src/kcuts.cpp:35-60); the plan from build_execution_graph +
+export_plan (proj/src/execgraph.cpp:295-361).  Values are execute_numeric's node loop
+(proj/src/simulator.cpp:77-127) run by the reference library itself (ref_driver Session).
 
-For every case: the reference planner's plan JSON (build_execution_graph + export_plan,
-execgraph.cpp:295-361), the reference's per-op graph_cost (cost.cpp:244-253), its
-execute_numeric result (simulator.cpp:55-149), and the fp64 value of every node of the
-reference's tiled CPU execution (via oracle/ref_driver.cpp's session, which runs
-execute_numeric's node loop through the reference's own dense.cpp kernels).
+Files per case  <name>.<mode>.k<k>.s<seed>.plan.json.gz   the plan document (wire format)
+                <name>.<mode>.k<k>.s<seed>.values.npz     fp64 values:
+  small plans (<= SMALL total node elements): "node:<id>" for every node and
+                                              "serial:<tensor>" (serial_execute)
+  larger plans: "summary:<holder id>" = [sum, sum|v|, sum v^2, v.flat[linspace(0, n-1, 61)]]
+                for every holder node.
 
-Cases mirror the reference's own test corpus (proj/tests/corpus.hpp:58-103) at the seeds its
-tests use (test_plan.cpp:178-223 seeds 17 and 5, acceptance.cpp:277-293 seed 33), plus
-structure-preserving reductions of the BASELINE configs.
+Usage: python tools/make_golden.py [--check]   (--check regenerates in memory and compares)
 """
 from __future__ import annotations
 
 import gzip
+import io
 import json
 import os
 import sys
@@ -26,103 +31,124 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle import ref  # noqa: E402
 
-OUT = os.path.join(ROOT, "tests", "golden")
-
-
-def corpus():
-    """proj/tests/corpus.hpp:58-103."""
-    out = []
-    for depth in range(1, 5):
-        out.append((f"mlp_train_d{depth}", ref.gen_mlp(8, [8] * (depth + 1), True, True)))
-    out.append(("mlp_fwd", ref.gen_mlp(16, [8, 8, 8], False, False)))
-    out.append(("mlp_rect", ref.gen_mlp(8, [8, 16, 8], True, False)))
-    out.append(("cnn_train", ref.gen_cnn(8, (6, 6), [2, 4], (3, 3), True)))
-    out.append(("cnn_fwd2", ref.gen_cnn(16, (8, 8), [4, 4, 8], (3, 3), False)))
-    return out
-
-
-def reduced_baselines():
-    """BASELINE configs with the same layer structure at CPU-oracle-friendly extents."""
-    return [
-        ("cfg1_mlp3x1024_b64", ref.gen_mlp(64, [1024] * 4, True, True)),     # cfg1 full size
-        ("cfg2r_mlp5x256_b64", ref.gen_mlp(64, [256] * 6, True, True)),      # cfg2 structure
-        ("cfg5r_mlp3x512_b32", ref.gen_mlp(32, [512] * 4, True, True)),      # cfg5 structure
-        ("fcr_alexnet_b32", ref.gen_mlp(32, [576, 256, 256, 64], True, True)),  # AlexNet-FC shape
-        ("cnnr_train_b16", ref.gen_cnn(16, (10, 10), [4, 8, 8], (3, 3), True)),
-    ]
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+SMALL = 50_000
 
 
 def summary(v: np.ndarray) -> np.ndarray:
-    """Size-independent fingerprint of a block: sum, sum|x|, sum x^2 and 61 elements at
-    fixed flat positions (used for cases too large to store whole)."""
-    flat = v.reshape(-1)
-    idx = np.unique(np.linspace(0, max(flat.size - 1, 0), 61).astype(np.int64))
-    head = np.array([flat.sum(), np.abs(flat).sum(), (flat * flat).sum()])
-    return np.concatenate([head, flat[idx]]) if flat.size else head
+    f = v.ravel()
+    idx = np.linspace(0, f.size - 1, 61).astype(np.int64)
+    return np.concatenate([[f.sum(), np.abs(f).sum(), (f * f).sum()], f[idx]])
 
 
-def write_case(name, graph, mode, k, seed, keep_all_nodes=True):
-    plan = ref.plan(graph, mode, k)
-    P = json.loads(plan)
-    cost = ref.graph_cost(graph, mode, k)
-    num = ref.execute_numeric(plan, seed)
-    sess = ref.Session(plan, seed)
+def reduce_kat_graph() -> str:
+    """proj/tests/test_plan.cpp:191-203."""
+    return json.dumps({"ops": [{"attrs": {"transpose_a": False, "transpose_b": False}, "id": "mm",
+                                "inputs": ["x", "w"], "kind": "matmul", "output": "z"}],
+                       "tensors": [{"dtype_bytes": 4, "id": "w", "role": "weight", "shape": [4, 4]},
+                                   {"dtype_bytes": 4, "id": "x", "role": "input", "shape": [4, 4]},
+                                   {"dtype_bytes": 4, "id": "z", "role": "activation", "shape": [4, 4]}]})
+
+
+def graphs() -> dict:
+    """Corpus graphs (proj/tests/corpus.hpp:58-103) and reduced BASELINE configs (same
+    structure as cfg1/cfg2/cfg5/AlexNet-FC/conv, smaller extents so the fp64 reference
+    finishes in seconds)."""
+    g = {}
+    for d in (1, 2, 3, 4):  # corpus.hpp:58-69 (train MLPs, width 8, batch 8)
+        g[f"mlp_train_d{d}"] = ref.gen_mlp(8, [8] * (d + 1))
+    g["mlp_fwd"] = ref.gen_mlp(16, [8, 8, 8], backward=False, update=False)     # corpus.hpp:70-76
+    g["mlp_rect"] = ref.gen_mlp(8, [8, 16, 8], update=False)                            # corpus.hpp:78-86
+    g["cnn_train"] = ref.gen_cnn(8, (6, 6), [2, 4], (3, 3), backward=True)      # corpus.hpp:90-95
+    g["cnn_fwd2"] = ref.gen_cnn(16, (8, 8), [4, 4, 8], (3, 3), backward=False)  # corpus.hpp:96-101
+    g["cfg1_mlp3x1024_b64"] = ref.gen_mlp(64, [1024] * 4)     # BASELINE configs[0], full size
+    g["cfg2r_mlp5x256_b64"] = ref.gen_mlp(64, [256] * 6)      # configs[1] structure, reduced
+    g["cfg5r_mlp3x512_b32"] = ref.gen_mlp(32, [512] * 4)      # configs[4] structure, reduced
+    g["fcr_alexnet_b32"] = ref.gen_mlp(32, [576, 256, 256, 64])  # AlexNet FC6-8 structure
+    g["cnnr_train_b16"] = ref.gen_cnn(16, (10, 10), [4, 8, 8], (3, 3), backward=True)
+    g["reduce_kat"] = reduce_kat_graph()
+    return g
+
+
+REDUCE_KAT_ASSIGN = json.dumps({"k": 1, "tilings": {"x": "C", "w": "R", "z": "R"}})
+
+
+def cases():
+    """(name, mode, k, seed).  Corpus: acceptance.cpp:277-293 ({data, model, opt} x k in {1,2},
+    seed 33) + hybrid, and test_plan.cpp:178-189 (kcuts k=2, seed 17)."""
+    out = []
+    corpus = ["mlp_train_d1", "mlp_train_d2", "mlp_train_d3", "mlp_train_d4", "mlp_fwd",
+              "mlp_rect", "cnn_train", "cnn_fwd2"]
+    for name in corpus:
+        for mode in ("data", "model", "opt"):
+            for k in (1, 2):
+                out.append((name, mode, k, 33))
+        out.append((name, "hybrid", 2, 33))
+        out.append((name, "opt", 2, 17))
+    for name in ("cfg1_mlp3x1024_b64", "cfg2r_mlp5x256_b64", "cfg5r_mlp3x512_b32", "fcr_alexnet_b32"):
+        for k in (0, 1, 2, 3):
+            out.append((name, "opt", k, 7))
+        for k in (1, 2, 3):
+            out.append((name, "data", k, 7))
+    for k in (0, 1, 2):
+        out.append(("cnnr_train_b16", "opt", k, 7))
+    for k in (1, 2):
+        out.append(("cnnr_train_b16", "data", k, 7))
+    out.append(("reduce_kat", "custom", 1, 5))
+    return out
+
+
+def file_stem(name, mode, k, seed):
+    return f"{name}.{mode}.k{k}.s{seed}"
+
+
+def make_case(gjson: str, name: str, mode: str, k: int, seed: int):
+    m = REDUCE_KAT_ASSIGN if mode == "custom" else mode
+    plan_text = ref.plan(gjson, m, k)
+    P = json.loads(plan_text)
+    sess = ref.Session(plan_text, seed)
+    total = sum(int(np.prod([hi - lo for lo, hi in n["region"]])) for n in P["nodes"])
     arrays = {}
-    holder_ids = {h for hs in P["holders"].values() for h in hs}
-    for n in P["nodes"]:
-        if keep_all_nodes:
+    if total <= SMALL:
+        for n in P["nodes"]:
             arrays["node:" + n["id"]] = sess.node(n["id"])
-        elif n["id"] in holder_ids:
-            arrays["summary:" + n["id"]] = summary(sess.node(n["id"]))
-    if keep_all_nodes:
         for t in P["graph"]["tensors"]:
             arrays["serial:" + t["id"]] = sess.serial(t["id"])
+    else:
+        for hs in P["holders"].values():
+            for h in hs:
+                arrays["summary:" + h] = summary(sess.node(h))
     sess.close()
-    tag = f"{name}.{mode}.k{k}.s{seed}"
-    with gzip.open(os.path.join(OUT, tag + ".plan.json.gz"), "wt") as f:
-        f.write(plan)
-    np.savez_compressed(os.path.join(OUT, tag + ".values.npz"), **arrays)
-    meta = {"case": name, "mode": mode, "k": k, "seed": seed,
-            "execute_numeric": {kk: num[kk] for kk in ("max_abs", "max_rel", "values")},
-            "graph_cost": {"total_bytes": cost["total_bytes"],
-                           "per_op": {r["op"]: r["bytes"] for r in cost["per_op"]},
-                           "forms": {r["op"]: r["form"] for r in cost["per_op"]}},
-            "fetch_bytes_total": P["fetch_bytes_total"]}
-    return tag, meta
+    return plan_text, arrays
 
 
 def main():
-    ref.build()
-    os.makedirs(OUT, exist_ok=True)
-    index = {}
-    for name, g in corpus():
-        for k in (1, 2):
-            modes = ["data", "model", "opt"] + (["hybrid"] if k >= 2 else [])
-            for mode in modes:
-                tag, meta = write_case(name, g, mode, k, 33)
-                index[tag] = meta
-        tag, meta = write_case(name, g, "opt", 2, 17)   # test_plan.cpp:178-189
-        index[tag] = meta
-    for name, g in reduced_baselines():
-        for k in (0, 1, 2, 3):
-            for mode in (["opt", "data"] if k else ["opt"]):
-                if name.startswith("cnnr") and k == 3:
-                    continue
-                tag, meta = write_case(name, g, mode, k, 7, keep_all_nodes=False)
-                index[tag] = meta
-    # the reducing-form known-answer plan of test_plan.cpp:191-223 (x:C, w:R, z:R, seed 5)
-    g = json.dumps({"tensors": [
-        {"id": "x", "shape": [4, 4], "dtype_bytes": 4, "role": "input"},
-        {"id": "w", "shape": [4, 4], "dtype_bytes": 4, "role": "weight"},
-        {"id": "z", "shape": [4, 4], "dtype_bytes": 4, "role": "activation"}],
-        "ops": [{"id": "mm", "kind": "matmul", "inputs": ["x", "w"], "output": "z",
-                 "attrs": {"transpose_a": False, "transpose_b": False}}]})
-    a = json.dumps({"k": 1, "tilings": {"x": "C", "w": "R", "z": "R"}})
-    tag, meta = write_case("reduce_kat", g, a, 1, 5)
-    index[tag] = meta
-    with open(os.path.join(OUT, "index.json"), "w") as f:
-        json.dump(index, f, indent=1, sort_keys=True)
-    print(f"wrote {len(index)} cases to {OUT}")
+    check = "--check" in sys.argv
+    if not ref.build():
+        sys.exit("oracle/_ref is not built and /root/reference is absent")
+    gs = graphs()
+    os.makedirs(GOLDEN, exist_ok=True)
+    bad = 0
+    for name, mode, k, seed in cases():
+        stem = os.path.join(GOLDEN, file_stem(name, mode, k, seed))
+        plan_text, arrays = make_case(gs[name], name, mode, k, seed)
+        if check:
+            old = json.loads(gzip.open(stem + ".plan.json.gz", "rt").read())
+            z = np.load(stem + ".values.npz")
+            same = old == json.loads(plan_text) and set(z.keys()) == set(arrays) and all(
+                np.array_equal(z[key], arrays[key]) for key in arrays)
+            bad += not same
+            print(("ok  " if same else "DIFF"), os.path.basename(stem))
+            continue
+        with gzip.GzipFile(stem + ".plan.json.gz", "wb", mtime=0) as f:
+            f.write(plan_text.encode())
+        buf = io.BytesIO()
+        np.savez_compressed(buf, **arrays)
+        with open(stem + ".values.npz", "wb") as f:
+            f.write(buf.getvalue())
+        print("wrote", os.path.basename(stem))
+    if bad:
+        sys.exit(f"{bad} fixtures differ from the reference")
 
 
 if __name__ == "__main__":
