@@ -128,6 +128,21 @@ int tpx_gemm(const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs, const
              float* c, int64_t c_rs, int n_epi, const int* epi_ops, const float* epi_scales,
              const float* const* epi_other, const int64_t* epi_other_rs, float* const* epi_out,
              const int64_t* epi_out_rs, int precision, uint64_t cuda_stream);
+/* tpx_gemm with the problem prepared once: `warmup` untimed runs, then `iters` runs timed with
+ * CUDA events on `cuda_stream`; *avg_ms = mean device time per run (iters > 0). */
+int tpx_gemm_timed(const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs, const float* b,
+                   int64_t b_rows, int64_t b_cols, int64_t b_rs, int transpose_a, int transpose_b,
+                   float* c, int64_t c_rs, int n_epi, const int* epi_ops, const float* epi_scales,
+                   const float* const* epi_other, const int64_t* epi_other_rs, float* const* epi_out,
+                   const int64_t* epi_out_rs, int precision, uint64_t cuda_stream, int warmup,
+                   int iters, double* avg_ms);
+/* Host-only: the persistent GEMM's tile schedule for `nprob` problems of P x Q x K (kernel
+ * orientation, 128 x bn tiles, 32-deep k-blocks) on `num_sms` SMs.  segs (8 int32 per segment:
+ * prob, tp, tq, kb0, kb1, kind, slot, n_parts) and seg_off (grid+1) are filled when large
+ * enough.  No GPU needed. */
+int tpx_gemm_schedule(int nprob, int P, int Q, int K, int bn, int num_sms, int force_groups,
+                      int* grid, int* nsegs, int* nslots, int* group, int* stream_k,
+                      int32_t* segs, int max_segs, int32_t* seg_off, int max_ctas);
 /* Debug: override the MN-major UMMA descriptor strides (bytes; 0 = defaults). */
 int tpx_debug_gemm_mn_desc(unsigned lbo, unsigned sbo);
 

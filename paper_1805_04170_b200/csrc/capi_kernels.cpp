@@ -1,7 +1,9 @@
 // Kernel-level C entry points (tpx_gemm) and the thread-local error slot shared by the ABI.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <string>
 
 #include "capi_util.h"
@@ -20,12 +22,12 @@ __attribute__((visibility("default"))) const char* tpx_last_error(void) {
 
 __attribute__((visibility("default"))) int tpx_version(void) { return 1; }
 
-__attribute__((visibility("default"))) int tpx_gemm(
+__attribute__((visibility("default"))) int tpx_gemm_timed(
     const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs, const float* b, int64_t b_rows,
     int64_t b_cols, int64_t b_rs, int transpose_a, int transpose_b, float* c, int64_t c_rs,
     int n_epi, const int* epi_ops, const float* epi_scales, const float* const* epi_other,
     const int64_t* epi_other_rs, float* const* epi_out, const int64_t* epi_out_rs, int precision,
-    uint64_t cuda_stream) {
+    uint64_t cuda_stream, int warmup, int iters, double* avg_ms) {
   return tpx::guard([&] {
     if (n_epi < 0 || n_epi > tpx::kMaxEpi) tpx::fail("tpx_gemm: too many epilogue stages");
     tpx::GemmSpec s;
@@ -52,14 +54,80 @@ __attribute__((visibility("default"))) int tpx_gemm(
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     tpx::GemmLaunch g = tpx::gemm_prepare({s}, sms, precision == 1);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
     try {
-      tpx::gemm_run(g, st);
+      for (int i = 0; i < std::max(0, warmup); ++i) tpx::gemm_run(g, st);
+      if (iters > 0) {
+        CUDA_CHECK(cudaEventCreate(&e0));
+        CUDA_CHECK(cudaEventCreate(&e1));
+        CUDA_CHECK(cudaEventRecord(e0, st));
+        for (int i = 0; i < iters; ++i) tpx::gemm_run(g, st);
+        CUDA_CHECK(cudaEventRecord(e1, st));
+      } else {
+        tpx::gemm_run(g, st);
+      }
       CUDA_CHECK(cudaStreamSynchronize(st));
+      if (iters > 0 && avg_ms) {
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        *avg_ms = double(ms) / iters;
+      }
     } catch (...) {
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
       tpx::gemm_free(g);
       throw;
     }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
     tpx::gemm_free(g);
+  });
+}
+
+__attribute__((visibility("default"))) int tpx_gemm(
+    const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs, const float* b, int64_t b_rows,
+    int64_t b_cols, int64_t b_rs, int transpose_a, int transpose_b, float* c, int64_t c_rs,
+    int n_epi, const int* epi_ops, const float* epi_scales, const float* const* epi_other,
+    const int64_t* epi_other_rs, float* const* epi_out, const int64_t* epi_out_rs, int precision,
+    uint64_t cuda_stream) {
+  return tpx_gemm_timed(a, a_rows, a_cols, a_rs, b, b_rows, b_cols, b_rs, transpose_a, transpose_b, c,
+                        c_rs, n_epi, epi_ops, epi_scales, epi_other, epi_other_rs, epi_out, epi_out_rs,
+                        precision, cuda_stream, 0, 0, nullptr);
+}
+
+__attribute__((visibility("default"))) int tpx_gemm_schedule(int nprob, int P, int Q, int K, int bn,
+                                                             int num_sms, int force_groups,
+                                                             int* grid, int* nsegs, int* nslots,
+                                                             int* group, int* stream_k,
+                                                             int32_t* segs, int max_segs,
+                                                             int32_t* seg_off, int max_ctas) {
+  return tpx::guard([&] {
+    if (nprob < 1 || P < 1 || Q < 1 || K < 0 || num_sms < 1) tpx::fail("tpx_gemm_schedule: bad shape");
+    if (bn != 32 && bn != 64 && bn != 128 && bn != 256) tpx::fail("tpx_gemm_schedule: bad tile width");
+    std::vector<tpx::GemmProblem> probs(static_cast<size_t>(nprob));
+    for (auto& pr : probs) {
+      pr.P = P;
+      pr.Q = Q;
+      pr.K = K;
+      pr.tiles_p = (P + 127) / 128;
+      pr.tiles_q = (Q + bn - 1) / bn;
+      pr.kb_total = (K + 31) / 32;
+    }
+    tpx::GemmSchedule S = tpx::gemm_schedule(probs, bn, num_sms, force_groups);
+    *grid = S.grid;
+    *nsegs = int(S.segs.size());
+    *nslots = S.nslots;
+    *group = S.group;
+    *stream_k = S.stream_k ? 1 : 0;
+    if (segs && int(S.segs.size()) <= max_segs) {
+      for (size_t i = 0; i < S.segs.size(); ++i) {
+        const tpx::GemmSeg& g = S.segs[i];
+        const int32_t v[8] = {g.prob, g.tp, g.tq, g.kb0, g.kb1, g.kind, g.slot, g.n_parts};
+        std::memcpy(segs + 8 * i, v, sizeof(v));
+      }
+    }
+    if (seg_off && S.grid + 1 <= max_ctas + 1)
+      for (int i = 0; i <= S.grid; ++i) seg_off[i] = S.seg_off[size_t(i)];
   });
 }
 

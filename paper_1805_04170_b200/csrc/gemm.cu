@@ -1,12 +1,22 @@
-// tcgen05 tile GEMM (kind::tf32, fp32 storage).  See gemm.h.
+// Persistent tcgen05 tile GEMM (kind::tf32, fp32 storage).  See gemm.h.
 //
-// Per CTA: one 128 x BN output tile (optionally one K-split of it).  Warp roles:
-//   warp 0 lane 0  TMA producer    (cp.async.bulk.tensor -> 128B-swizzled smem ring)
-//   warp 1 lane 0  MMA issuer      (tcgen05.mma.cta_group::1.kind::tf32, accum in TMEM)
-//   warp 2         TMEM allocator  (BN fp32 columns x 128 lanes)
-//   warps 4..7     epilogue        (tcgen05.ld -> registers -> fused elementwise -> global)
-// Split-K partials go to a workspace; the last-arriving split (atomic ticket) sums all of
-// them in split order (deterministic) and runs the epilogue.
+// One CTA per SM, each walking a host-built list of segments (tile, k-block range).  Warp roles:
+//   warp 0 lane 0  TMA producer   (cp.async.bulk.tensor -> 128B-swizzled smem ring)
+//   warp 1 lane 0  MMA issuer     (tcgen05.mma.cta_group::1.kind::tf32 into one of two TMEM
+//                                  accumulators, so segment i+1's mainloop overlaps segment
+//                                  i's epilogue)
+//   warp 2         TMEM allocator (2 x BN fp32 columns x 128 lanes)
+//   warps 4..7     epilogue       (tcgen05.ld -> registers -> fused elementwise -> smem
+//                                  transpose -> coalesced global stores; the elementwise
+//                                  operand arrives by TMA one 32 x 32 box ahead)
+//   warps 8..11    3xTF32 operand split (SPLIT only)
+// Scheduling (gemm_prepare): whole tiles when there are many, else stream-K: the k-blocks of
+// all tiles are cut evenly over the CTAs.  A tile cut into several segments is finished by the
+// CTA holding its first k-range (the "head"); the others write partial tiles to a workspace and
+// raise a flag.  The head waits for those flags — they are always the producers' FIRST
+// segments, so no chain of waits can form — and adds the partials in k order, so the result is
+// deterministic.  CTA groups of G (= the P-tile count of a small-M problem) walk the same k
+// ranges side by side so a streamed B operand is read from DRAM once and from L2 G-1 times.
 #include "gemm.h"
 
 #include <cuda.h>
@@ -26,17 +36,32 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
+constexpr int CW = 16;                                    // epilogue chunk: 16 accumulator columns
+constexpr uint32_t kOutStage = 32 * CW * 4;               // one 32-row x CW fp32 box (64B swizzle)
+constexpr uint32_t kOutStageBytes = 8 * kOutStage;        // <= 8 epilogue warps x 1 transpose box
+constexpr uint32_t kOtherBytes = 8 * kOutStage;           // <= 8 epilogue warps x 1 operand box
+constexpr uint32_t kSmemMax = 232448;                     // 227 KB opt-in
+constexpr uint32_t kBarBytes = 512;
 
-// Operand bytes of one k-block; a split (3xTF32) stage also holds the low parts.
+enum SegKind : int { SEG_WHOLE = 0, SEG_HEAD = 1, SEG_PART = 2 };
+
 __host__ __device__ constexpr uint32_t operand_bytes(int bn) { return uint32_t(BM * BK * 4 + bn * BK * 4); }
 __host__ __device__ constexpr uint32_t stage_bytes(int bn, bool split) {
   return operand_bytes(bn) * (split ? 2u : 1u);
 }
-__host__ __device__ constexpr int stages_for(int bn, bool split) {
-  return int((192u * 1024u) / stage_bytes(bn, split)) > 8 ? 8 : int((192u * 1024u) / stage_bytes(bn, split));
+inline int stages_for(int bn, bool split, bool other) {
+  const uint32_t budget = kSmemMax - 1024 - kBarBytes - kOutStageBytes - (other ? kOtherBytes : 0);
+  return std::min<int>(8, int(budget / stage_bytes(bn, split)));
 }
-constexpr size_t smem_for(int bn, bool split) {
-  return size_t(stages_for(bn, split)) * stage_bytes(bn, split) + 1024 + 256;
+inline size_t smem_for(int bn, bool split, bool other, int stages) {
+  return size_t(stages) * stage_bytes(bn, split) + kOutStageBytes + (other ? kOtherBytes : 0) + 1024 + kBarBytes;
+}
+// 12 warps: producer, MMA, TMEM allocator, spare, then 8 epilogue warps (two per TMEM lane
+// quarter, each on half the tile's columns) -- or, for 3xTF32, 4 epilogue + 4 splitting warps.
+__host__ __device__ constexpr int threads_for(bool split) { return 384; }
+__host__ __device__ constexpr int epi_warps(bool split) { return split ? 4 : 8; }
+__host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
+  return 2 * bn <= 32 ? 32 : 2 * bn <= 64 ? 64 : 2 * bn <= 128 ? 128 : 2 * bn <= 256 ? 256 : 512;
 }
 
 __device__ __forceinline__ float tf32_rna(float x) {
@@ -45,71 +70,155 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
-__device__ __forceinline__ float epi_apply(int op, float prev, float other, float s) {
+// One fused elementwise stage over a thread's 32 values (the op is uniform per problem, so
+// the switch sits outside the element loop).
+__device__ __forceinline__ void epi_apply(int op, float (&v)[CW], const float (&o)[CW], float s) {
   switch (op) {
-    case EPI_TANH: return tanhf(prev);
-    case EPI_DTANH: {
-      float t = tanhf(prev);
-      return 1.0f - t * t;
-    }
-    case EPI_SCALE: return s * prev;
-    case EPI_ADD: return prev + other;
-    case EPI_SUB_PO: return prev - other;
-    case EPI_SUB_OP: return other - prev;
-    default: return prev;
+    case EPI_TANH:
+#pragma unroll
+      for (int j = 0; j < CW; ++j) v[j] = tanhf(v[j]);
+      break;
+    case EPI_DTANH:
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const float t = tanhf(v[j]);
+        v[j] = 1.0f - t * t;
+      }
+      break;
+    case EPI_SCALE:
+#pragma unroll
+      for (int j = 0; j < CW; ++j) v[j] = s * v[j];
+      break;
+    case EPI_ADD:
+#pragma unroll
+      for (int j = 0; j < CW; ++j) v[j] = v[j] + o[j];
+      break;
+    case EPI_SUB_PO:
+#pragma unroll
+      for (int j = 0; j < CW; ++j) v[j] = v[j] - o[j];
+      break;
+    case EPI_SUB_OP:
+#pragma unroll
+      for (int j = 0; j < CW; ++j) v[j] = o[j] - v[j];
+      break;
+    default: break;
   }
 }
 
 __device__ __forceinline__ bool epi_needs_other(int op) { return op >= EPI_ADD; }
 
-// Store 32 consecutive columns [q0, q0+32) of row p.
+// Store CW consecutive columns [q0, q0+CW) of row p.  Used for swapped problems (rs == 1):
+// the warp's 32 rows are 32 consecutive floats, so every scalar store is one 128-byte line.
 __device__ __forceinline__ void store_chunk(float* base, long long rs, long long cs, int p,
-                                            int q0, int P, int Q, const float (&v)[32]) {
+                                            int q0, int P, int Q, const float (&v)[CW]) {
   if (p >= P) return;
   float* row = base + (long long)p * rs;
-  if (cs == 1 && q0 + 32 <= Q && ((reinterpret_cast<uintptr_t>(row + q0) & 15) == 0)) {
+  if (cs == 1 && q0 + CW <= Q && ((reinterpret_cast<uintptr_t>(row + q0) & 15) == 0)) {
     float4* d = reinterpret_cast<float4*>(row + q0);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) d[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    for (int j = 0; j < CW / 4; ++j) d[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
   } else {
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
+    for (int j = 0; j < CW; ++j)
       if (q0 + j < Q) row[(long long)(q0 + j) * cs] = v[j];
   }
 }
 
 __device__ __forceinline__ void load_chunk(const float* base, long long rs, long long cs, int p,
-                                           int q0, int P, int Q, float (&v)[32]) {
+                                           int q0, int P, int Q, float (&v)[CW]) {
   if (p >= P) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    for (int j = 0; j < CW; ++j) v[j] = 0.f;
     return;
   }
   const float* row = base + (long long)p * rs;
-  if (cs == 1 && q0 + 32 <= Q && ((reinterpret_cast<uintptr_t>(row + q0) & 15) == 0)) {
+  if (cs == 1 && q0 + CW <= Q && ((reinterpret_cast<uintptr_t>(row + q0) & 15) == 0)) {
     const float4* s = reinterpret_cast<const float4*>(row + q0);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < CW / 4; ++j) {
       float4 t = __ldg(s + j);
       v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = (q0 + j < Q) ? __ldg(row + (long long)(q0 + j) * cs) : 0.f;
+    for (int j = 0; j < CW; ++j) v[j] = (q0 + j < Q) ? __ldg(row + (long long)(q0 + j) * cs) : 0.f;
   }
 }
 
+// Byte offset of 16-byte chunk c of row r in a 32 x CW fp32 box with the TMA 64-byte swizzle
+// (chunk index XOR address bits 7..8): conflict-free both row-wise and column-wise.
+__device__ __forceinline__ uint32_t box_off(int r, int c) { return r * (CW * 4) + ((c ^ ((r >> 1) & 3)) << 4); }
+
+__device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 r;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a) : "memory");
+  return r;
+}
+
+// Store a warp's 32 x CW block (thread = row `lane`, CW consecutive columns) into a row-major
+// global view, transposed through a swizzled smem box so that each warp store instruction
+// writes 8 rows x 64 contiguous bytes.  Rows >= P and columns >= Q are masked.
+__device__ __forceinline__ void store_block(uint32_t sbuf, int lane, const float (&v)[CW], float* base,
+                                            long long rs, int prow0, int q0, int P, int Q, bool stream) {
+#pragma unroll
+  for (int j = 0; j < CW / 4; ++j) sts128(sbuf + box_off(lane, j), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  __syncwarp();
+  const int c = lane & 3;
+  const int gq = q0 + c * 4;
+  const bool vec = ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && ((rs & 3) == 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = i * 8 + (lane >> 2);
+    const float4 x = lds128(sbuf + box_off(r, c));
+    const int gp = prow0 + r;
+    if (gp < P) {
+      float* dst = base + (long long)gp * rs + gq;
+      if (vec && gq + 4 <= Q) {
+        if (stream) __stcs(reinterpret_cast<float4*>(dst), x);  // evict-first: not re-read soon
+        else *reinterpret_cast<float4*>(dst) = x;
+      } else {
+        if (gq < Q) dst[0] = x.x;
+        if (gq + 1 < Q) dst[1] = x.y;
+        if (gq + 2 < Q) dst[2] = x.z;
+        if (gq + 3 < Q) dst[3] = x.w;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void flag_release(unsigned* f) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(1u) : "memory");
+}
+__device__ __forceinline__ unsigned flag_acquire(const unsigned* f) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+
+// Partial tiles live in L2-resident workspace slots of BM x BN floats, interleaved so that one
+// warp-wide float4 access (32 rows, same 4 columns) is 512 contiguous bytes.
+__device__ __forceinline__ float4* ws_ptr(float* ws, int slot, int bn, int c0, int j, int row) {
+  return reinterpret_cast<float4*>(ws + (size_t)slot * BM * bn) + ((c0 / CW) * (CW / 4) + j) * BM + row;
+}
+
 // SPLIT = 3xTF32: every fp32 operand x = hi + lo with hi = tf32_rna(x), lo = x - hi (exact);
-// D += lo_A*hi_B + hi_A*lo_B + hi_A*hi_B.  The split is done in shared memory by warps 2..7
-// (idle during the mainloop) between the TMA landing and the MMA issue.
+// D += lo_A*hi_B + hi_A*lo_B + hi_A*hi_B.  The split runs in shared memory between the TMA
+// landing and the MMA issue (warps 8..11).
 template <int BN, bool P_MN, bool Q_MN, bool SPLIT>
-__global__ void __launch_bounds__(256, 1)
-    gemm_tf32_kernel(const GemmProblem* __restrict__ probs, int nprob) {
-  constexpr int STAGES = stages_for(BN, SPLIT);
+__global__ void __launch_bounds__(threads_for(SPLIT), 1)
+    gemm_tf32_kernel(const GemmProblem* __restrict__ probs, const GemmSeg* __restrict__ segs,
+                     const int* __restrict__ seg_off, float* __restrict__ ws,
+                     unsigned* __restrict__ flags, const int STAGES, const int PF,
+                     const int has_other) {
   constexpr uint32_t A_BYTES = BM * BK * 4;
   constexpr uint32_t OPB = operand_bytes(BN);
   constexpr uint32_t STAGE = stage_bytes(BN, SPLIT);
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
+  constexpr int NEPI = epi_warps(SPLIT);
   constexpr uint32_t IDESC = (1u << 4)                 // D format f32
                              | (2u << 7) | (2u << 10)  // A, B format tf32
                              | (uint32_t(P_MN) << 15) | (uint32_t(Q_MN) << 16) |
@@ -118,37 +227,30 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint8_t* out_stage = smem + STAGES * STAGE;  // [4 warps][32 rows x 128 B] store transpose
+  uint8_t* other_stage = out_stage + kOutStageBytes;  // [8 warps][32 rows x 64 B] if has_other
+  uint64_t* full = reinterpret_cast<uint64_t*>(other_stage + ((has_other & 1) ? kOtherBytes : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* split_done = empty + STAGES;
-  uint64_t* tmem_full = split_done + STAGES;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
+  uint64_t* tmem_full = split_done + STAGES;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;       // [2]
+  uint64_t* other_bar = tmem_empty + 2;       // [8] one per epilogue warp
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(other_bar + 8);
 
-  int pi = 0;
-  const int u = blockIdx.x;
-  while (pi + 1 < nprob && probs[pi + 1].unit_begin <= u) ++pi;
-  const GemmProblem& pr = probs[pi];
-  const int local = u - pr.unit_begin;
-  const int ks = local % pr.splits;
-  const int t = local / pr.splits;
-  const int tq = t % pr.tiles_q;
-  const int tp = t / pr.tiles_q;
-  const int kb0 = ks * pr.kb_per_split;
-  const int kb1 = min(pr.kb_total, kb0 + pr.kb_per_split);
-  const int nkb = kb1 - kb0;
-
+  const int s_begin = seg_off[blockIdx.x], s_end = seg_off[blockIdx.x + 1];
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&split_done[s], 6);  // one arrival per splitting warp
+      mbar_init(&split_done[s], 4);  // one arrival per splitting warp
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], NEPI);  // one arrival per epilogue warp
+    }
+    for (int w = 0; w < 8; ++w) mbar_init(&other_bar[w], 1);
     fence_barrier_init();
-    tma_prefetch_desc(pr.tmap_a);
-    tma_prefetch_desc(pr.tmap_b);
   }
   if (warp == 2) tmem_alloc(tmem_holder, TMEM_COLS);
   tc_fence_before();
@@ -156,160 +258,278 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  // One k-block of operands: K-major tiles are one 2-D box; MN-major tiles are 32-wide
+  // 128B_BASE32B-swizzled chunks 4096 bytes apart, one 3-D box when the extent allows.
+  auto load_kblock = [&](const GemmProblem& pr, int kb, int p0, int q0, uint8_t* sa, uint8_t* sb,
+                         uint64_t* bar, uint64_t pol_a, uint64_t pol_b) {
+    const int k0 = kb * BK;
+    if constexpr (!P_MN) {
+      tma_load_2d_hint(sa, pr.tmap_a, bar, k0, p0, pol_a);
+    } else if (pr.a3d) {
+      tma_load_3d_hint(sa, pr.tmap_a, bar, 0, k0, p0 / 32, pol_a);
+    } else {
+#pragma unroll
+      for (int j = 0; j < BM / 32; ++j) tma_load_2d_hint(sa + j * 4096, pr.tmap_a, bar, p0 + 32 * j, k0, pol_a);
+    }
+    if constexpr (!Q_MN) {
+      tma_load_2d_hint(sb, pr.tmap_b, bar, k0, q0, pol_b);
+    } else if (pr.b3d) {
+      tma_load_3d_hint(sb, pr.tmap_b, bar, 0, k0, q0 / 32, pol_b);
+    } else {
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j) tma_load_2d_hint(sb + j * 4096, pr.tmap_b, bar, q0 + 32 * j, k0, pol_b);
+    }
+  };
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
-    const int p0 = tp * BM, q0 = tq * BN;
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % STAGES;
-      const uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      uint8_t* sa = smem + s * STAGE;
-      uint8_t* sb = sa + A_BYTES;
-      mbar_arrive_expect_tx(&full[s], OPB);
-      const int k0 = (kb0 + i) * BK;
-      if constexpr (!P_MN) {
-        tma_load_2d(sa, pr.tmap_a, &full[s], k0, p0);
-      } else {
-#pragma unroll
-        for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 4096, pr.tmap_a, &full[s], p0 + 32 * j, k0);
-      }
-      if constexpr (!Q_MN) {
-        tma_load_2d(sb, pr.tmap_b, &full[s], k0, q0);
-      } else {
-#pragma unroll
-        for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, pr.tmap_b, &full[s], q0 + 32 * j, k0);
+    const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+    uint32_t s = 0, ph = 0;  // ring slot and its phase parity
+    for (int si = s_begin; si < s_end; ++si) {
+      const GemmSeg sg = segs[si];
+      const GemmProblem& pr = probs[sg.prob];
+      const int p0 = sg.tp * BM, q0 = sg.tq * BN;
+      const uint64_t pol_a = pr.a_stream ? stream : keep, pol_b = pr.b_stream ? stream : keep;
+      for (int kb = sg.kb0; kb < sg.kb1; ++kb, (++s == uint32_t(STAGES)) ? (s = 0, ph ^= 1) : 0) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * STAGE;
+        mbar_arrive_expect_tx(&full[s], OPB);
+        load_kblock(pr, kb, p0, q0, sa, sa + A_BYTES, &full[s], pol_a, pol_b);
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread)
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % STAGES;
-      const uint32_t ph = (i / STAGES) & 1;
-      if constexpr (SPLIT) mbar_wait(&split_done[s], ph);
-      else mbar_wait(&full[s], ph);
+    uint32_t s = 0, ph = 0;  // ring slot and its phase parity
+    for (int si = s_begin, i = 0; si < s_end; ++si, ++i) {
+      const GemmSeg sg = segs[si];
+      const GemmProblem& pr = probs[sg.prob];
+      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+      mbar_wait(&tmem_empty[acc], aph ^ 1);
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + s * STAGE);
-      const uint32_t sb = sa + A_BYTES;
+      const uint32_t d = tmem_base + acc * BN;
+      for (int kb = sg.kb0; kb < sg.kb1; ++kb, (++s == uint32_t(STAGES)) ? (s = 0, ph ^= 1) : 0) {
+        if constexpr (SPLIT) mbar_wait(&split_done[s], ph);
+        else mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * STAGE);
+        const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-      for (int kk = 0; kk < BK / 8; ++kk) {
-        // K-major: 128B rows of K, 8-row atoms (SBO 1024), K step = +32 bytes.
-        // MN-major: 128B rows of M/N per k, 32-byte-granule swizzle, 4-row groups (SBO 512),
-        //           32-column chunks 4096 bytes apart (LBO), K step = 8 rows = +1024 bytes.
-        const uint64_t ad = P_MN ? umma_desc(sa + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1)
-                                 : umma_desc(sa + kk * 32, 16, 1024, 2);
-        const uint64_t bd = Q_MN ? umma_desc(sb + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1)
-                                 : umma_desc(sb + kk * 32, 16, 1024, 2);
-        if constexpr (SPLIT) {
-          // low parts live OPB bytes after the high parts, in the same (swizzled) layout
-          const uint64_t lo = uint64_t((OPB >> 4) & 0x3FFFu);
-          mma_tf32(tmem_base, ad + lo, bd, IDESC, (i > 0 || kk > 0) ? 1u : 0u);
-          mma_tf32(tmem_base, ad, bd + lo, IDESC, 1u);
-          mma_tf32(tmem_base, ad, bd, IDESC, 1u);
-        } else {
-          mma_tf32(tmem_base, ad, bd, IDESC, (i > 0 || kk > 0) ? 1u : 0u);
-        }
-      }
-      mma_commit(&empty[s]);
-    }
-    mma_commit(tmem_full);
-  }
-  if (SPLIT && warp >= 2) {
-    // ---------------- 3xTF32 split: hi in place, lo into the stage's second half
-    const int tid = threadIdx.x - 64;  // 0..191
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % STAGES;
-      const uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(&full[s], ph);
-      float4* hi = reinterpret_cast<float4*>(smem + s * STAGE);
-      float4* lo = reinterpret_cast<float4*>(smem + s * STAGE + OPB);
-      for (int c = tid; c < int(OPB / 16); c += 192) {
-        float4 x = hi[c], h, l;
-        h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
-        l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
-        hi[c] = h;
-        lo[c] = l;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&split_done[s]);
-    }
-  }
-  if (warp >= 4) {
-    // ---------------- epilogue warpgroup
-    const int ew = warp - 4;
-    const int row = ew * 32 + lane;
-    const int p = tp * BM + row;
-    const uint32_t taddr_row = tmem_base + (uint32_t(ew * 32) << 16);
-    if (nkb > 0) mbar_wait(tmem_full, 0);
-    tc_fence_after();
-
-    const int splits = pr.splits;
-    float* ws_tile = nullptr;
-    if (splits > 1) {
-      ws_tile = pr.ws + (size_t)t * splits * BM * BN;
-      float* mine = ws_tile + ((size_t)ks * BM + row) * BN;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        if (nkb > 0) {
-          tmem_ld32(taddr_row + c0, v);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
-        }
-        float4* d = reinterpret_cast<float4*>(mine + c0);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) __stcg(d + j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-      }
-      __threadfence();
-      named_bar_sync(1, 128);
-      if (row == 0) {
-        const unsigned old = atomicAdd(&pr.counters[t], 1u);
-        const int is_last = old == unsigned(splits - 1);
-        if (is_last) pr.counters[t] = 0;
-        *last_flag = is_last;
-      }
-      named_bar_sync(1, 128);
-      if (!*last_flag) goto done;
-      __threadfence();
-    }
-
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      if (splits > 1) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
-        for (int s = 0; s < splits; ++s) {
-          const float4* src = reinterpret_cast<const float4*>(ws_tile + ((size_t)s * BM + row) * BN + c0);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4 x = __ldcg(src + j);
-            v[4 * j] += x.x; v[4 * j + 1] += x.y; v[4 * j + 2] += x.z; v[4 * j + 3] += x.w;
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          // K-major: 128B rows of K, 8-row atoms (SBO 1024), K step = +32 bytes.
+          // MN-major: 128B rows of M/N per k, 32-byte-granule swizzle, 4-row groups (SBO 512),
+          //           32-column chunks 4096 bytes apart (LBO), K step = 8 rows = +1024 bytes.
+          const uint64_t ad = P_MN ? umma_desc(sa + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1)
+                                   : umma_desc(sa + kk * 32, 16, 1024, 2);
+          const uint64_t bd = Q_MN ? umma_desc(sb + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1)
+                                   : umma_desc(sb + kk * 32, 16, 1024, 2);
+          const uint32_t accum = (kb > sg.kb0 || kk > 0) ? 1u : 0u;
+          if constexpr (SPLIT) {
+            // low parts live OPB bytes after the high parts, in the same (swizzled) layout
+            const uint64_t lo = uint64_t((OPB >> 4) & 0x3FFFu);
+            mma_tf32(d, ad + lo, bd, IDESC, accum);
+            mma_tf32(d, ad, bd + lo, IDESC, 1u);
+            mma_tf32(d, ad, bd, IDESC, 1u);
+          } else {
+            mma_tf32(d, ad, bd, IDESC, accum);
           }
         }
-      } else if (nkb > 0) {
-        tmem_ld32(taddr_row + c0, v);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        mma_commit(&empty[s]);
       }
-      const int q0 = tq * BN + c0;
-      if (q0 >= pr.Q) continue;
-      store_chunk(pr.out, pr.out_rs, pr.out_cs, p, q0, pr.P, pr.Q, v);
-      for (int e = 0; e < pr.n_epi; ++e) {
-        const EpiStage& st = pr.epi[e];
-        float o[32];
-        if (epi_needs_other(st.op)) {
-          load_chunk(st.other, st.o_rs, st.o_cs, p, q0, pr.P, pr.Q, o);
+      mma_commit(&tmem_full[acc]);
+    }
+  } else if (SPLIT && warp >= 8) {  // (SPLIT: NEPI == 4, epilogue warps 4..7)
+    // ---------------- 3xTF32 split: hi in place, lo into the stage's second half
+    const int tid = threadIdx.x - 256;  // 0..127
+    uint32_t s = 0, ph = 0;  // ring slot and its phase parity
+    for (int si = s_begin; si < s_end; ++si) {
+      const GemmSeg sg = segs[si];
+      for (int kb = sg.kb0; kb < sg.kb1; ++kb, (++s == uint32_t(STAGES)) ? (s = 0, ph ^= 1) : 0) {
+        mbar_wait(&full[s], ph);
+        float4* hi = reinterpret_cast<float4*>(smem + s * STAGE);
+        float4* lo = reinterpret_cast<float4*>(smem + s * STAGE + OPB);
+        for (int c = tid; c < int(OPB / 16); c += 128) {
+          float4 x = hi[c], h, l;
+          h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
+          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+          hi[c] = h;
+          lo[c] = l;
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&split_done[s]);
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + NEPI) {
+    // ---------------- epilogue: warp 4+e owns TMEM lanes [32(e%4), +32) and, with 8 warps,
+    // the columns [ (e/4) BN/2, (e/4+1) BN/2 )
+    const int ew = warp - 4;
+    const int lq = ew & 3;
+    const int c_begin = NEPI == 8 ? (ew >> 2) * (BN / 2) : 0;
+    const int c_end = NEPI == 8 ? c_begin + BN / 2 : BN;
+    const int row = lq * 32 + lane;
+    const bool leader = (ew == 0 && lane == 0);
+    uint32_t o_used = 0;  // operand boxes consumed by this warp
+    const uint64_t o_policy = policy_evict_first();  // the elementwise operand is read once
+    // Request the operand box of the first chunk at or after (si, c0) that consumes one.
+    auto issue_other = [&](int si, int c0) {
+      if (!(has_other & 1)) return;
+      for (; si < s_end; ++si, c0 = c_begin) {
+        const GemmSeg sg = segs[si];
+        if (sg.kind == SEG_PART) continue;
+        const GemmProblem& pr = probs[sg.prob];
+        if (!pr.tmap_other || pr.other_stage < 0) continue;
+        if (c0 < c_end && sg.tq * BN + c0 < pr.Q) {
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&other_bar[ew], kOutStage);
+          tma_load_2d_hint(other_stage + ew * kOutStage, pr.tmap_other, &other_bar[ew], sg.tq * BN + c0,
+                           sg.tp * BM + lq * 32, o_policy);
+          return;
+        }
+      }
+    };
+    if (lane == 0) issue_other(s_begin, c_begin);
+    for (int si = s_begin, i = 0; si < s_end; ++si, ++i) {
+      const GemmSeg sg = segs[si];
+      const GemmProblem& pr = probs[sg.prob];
+      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+      const bool have = sg.kb1 > sg.kb0;
+      const uint32_t taddr = tmem_base + acc * BN + (uint32_t(lq * 32) << 16);
+      if (has_other & 2) mbar_wait_sleep(&tmem_full[acc], aph);
+      else mbar_wait(&tmem_full[acc], aph);
+      tc_fence_after();
+
+      if (sg.kind == SEG_PART) {
+#pragma unroll 1
+        for (int c0 = c_begin; c0 < c_end; c0 += CW) {
+          float v[CW];
+          if (have) {
+            tmem_ld16(taddr + c0, v);
+          } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = epi_apply(st.op, v[j], epi_needs_other(st.op) ? o[j] : 0.f, st.scale);
-        store_chunk(st.out, st.out_rs, st.out_cs, p, q0, pr.P, pr.Q, v);
+            for (int j = 0; j < CW; ++j) v[j] = 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < CW / 4; ++j)
+            __stcg(ws_ptr(ws, sg.slot, BN, c0, j, row), make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+        __threadfence();
+        named_bar_sync(1, NEPI * 32);
+        if (leader) flag_release(&flags[sg.slot]);
+        continue;
+      }
+
+      if (sg.kind == SEG_HEAD) {
+        if (leader) {
+          for (int j = 0; j < sg.n_parts; ++j) {
+            unsigned* f = &flags[sg.slot + j];
+            long long t0 = clock64();
+            uint32_t spins = 0;
+            while (flag_acquire(f) == 0u) {
+              if ((++spins & 1023u) == 0 && clock64() - t0 > (1ll << 35)) __trap();
+            }
+            *f = 0u;  // re-arm for the next launch (stream order separates launches)
+          }
+          __threadfence();
+        }
+        named_bar_sync(1, NEPI * 32);
+      }
+
+      const int p = sg.tp * BM + row;
+      const int prow0 = sg.tp * BM + lq * 32;
+      // needs-other stage (w_next = w - wd): its operand is fetched before the TMEM drain
+      const int oe = pr.other_stage;
+      const void* omap = pr.tmap_other;
+      const bool o_tma = omap != nullptr;
+      const uint32_t sbuf = smem_u32(out_stage + ew * kOutStage);
+      // epilogue descriptors in registers for the whole segment (the chunk loop stores through
+      // generic pointers, so the compiler would otherwise re-load them from global per chunk)
+      const int nout = 1 + pr.n_epi;
+      float* obase[1 + kMaxEpi];
+      int ors[1 + kMaxEpi], ocs[1 + kMaxEpi];  // element strides (host checks < 2^31)
+      int eop[kMaxEpi];
+      float esc[kMaxEpi];
+      obase[0] = pr.out; ors[0] = int(pr.out_rs); ocs[0] = int(pr.out_cs);
+#pragma unroll
+      for (int e = 0; e < kMaxEpi; ++e) {
+        const bool on = e < pr.n_epi;
+        obase[1 + e] = on ? pr.epi[e].out : nullptr;
+        ors[1 + e] = on ? int(pr.epi[e].out_rs) : 0;
+        ocs[1 + e] = on ? int(pr.epi[e].out_cs) : 0;
+        eop[e] = on ? pr.epi[e].op : EPI_NONE;
+        esc[e] = on ? pr.epi[e].scale : 0.f;
+      }
+      const int PP = pr.P, QQ = pr.Q;
+      const bool ostream = pr.out_stream != 0;
+#pragma unroll 1
+      for (int c0 = c_begin; c0 < c_end; c0 += CW) {
+        const int q0 = sg.tq * BN + c0;
+        float o[CW];
+        if (oe >= 0 && q0 < QQ) {
+          if (o_tma) {
+            // the box was requested one chunk ahead; read my row, then request the next box
+            mbar_wait(&other_bar[ew], o_used & 1);
+            const uint32_t ob = smem_u32(other_stage + ew * kOutStage);
+#pragma unroll
+            for (int j = 0; j < CW / 4; ++j) {
+              const float4 x = lds128(ob + box_off(lane, j));
+              o[4 * j] = x.x; o[4 * j + 1] = x.y; o[4 * j + 2] = x.z; o[4 * j + 3] = x.w;
+            }
+            ++o_used;
+            __syncwarp();
+            if (lane == 0) {
+              if (c0 + CW < c_end && q0 + CW < QQ) {
+                fence_proxy_async_smem();  // same segment: the next box of this tile
+                mbar_arrive_expect_tx(&other_bar[ew], kOutStage);
+                tma_load_2d_hint(other_stage + ew * kOutStage, omap, &other_bar[ew], q0 + CW, prow0, o_policy);
+              } else {
+                issue_other(si + 1, c_begin);
+              }
+            }
+          } else {
+            load_chunk(pr.epi[oe].other, pr.epi[oe].o_rs, pr.epi[oe].o_cs, p, q0, PP, QQ, o);
+          }
+        }
+        float v[CW];
+        if (have) {
+          tmem_ld16(taddr + c0, v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) v[j] = 0.f;
+        }
+        if (c0 + CW >= c_end) {
+          // accumulator drained: hand it back to the MMA warp before the global traffic
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+        }
+        if (sg.kind == SEG_HEAD) {
+          for (int pp = 0; pp < sg.n_parts; ++pp) {
+#pragma unroll
+            for (int j = 0; j < CW / 4; ++j) {
+              const float4 x = __ldcg(ws_ptr(ws, sg.slot + pp, BN, c0, j, row));
+              v[4 * j] += x.x; v[4 * j + 1] += x.y; v[4 * j + 2] += x.z; v[4 * j + 3] += x.w;
+            }
+          }
+        }
+        if (q0 >= QQ) continue;
+#pragma unroll
+        for (int e = 0; e <= kMaxEpi; ++e) {
+          if (e >= nout) break;
+          if (e > 0) {
+            if (epi_needs_other(eop[e - 1]) && e - 1 != oe) {
+              const EpiStage& st = pr.epi[e - 1];
+              load_chunk(st.other, st.o_rs, st.o_cs, p, q0, PP, QQ, o);
+            }
+            epi_apply(eop[e - 1], v, o, esc[e - 1]);
+          }
+          if (ocs[e] == 1) store_block(sbuf, lane, v, obase[e], ors[e], prow0, q0, PP, QQ, ostream);
+          else store_chunk(obase[e], ors[e], ocs[e], p, q0, PP, QQ, v);  // swapped: lanes consecutive
+        }
       }
     }
   }
-done:
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -318,7 +538,7 @@ done:
   }
 }
 
-using KernelFn = void (*)(const GemmProblem*, int);
+using KernelFn = void (*)(const GemmProblem*, const GemmSeg*, const int*, float*, unsigned*, int, int, int);
 
 template <int BN, bool SPLIT>
 KernelFn pick(bool p_mn, bool q_mn) {
@@ -359,18 +579,35 @@ EncodeTiledFn encode_fn() {
 // 2-D fp32 tensor map over a row-major view: `inner` contiguous elements per row, `outer`
 // rows `row_stride` elements apart, boxes of box_inner x box_outer, 128-byte swizzle.
 void make_map(CUtensorMap* m, const float* base, long long inner, long long outer,
-              long long row_stride, int box_inner, int box_outer, bool mn_major) {
+              long long row_stride, int box_inner, int box_outer, bool mn_major, bool sw64 = false) {
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   cuuint64_t strides[1] = {(cuuint64_t)(std::max<long long>(row_stride, inner) * 4)};
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                           sw64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+// 3-D map of an MN-major operand whose MN extent is a multiple of 32: (32 MN elements, K rows,
+// MN/32 chunks), so one box of (32, 32, nchunk) lands as nchunk 4096-byte swizzled chunks.
+void make_map_mn3d(CUtensorMap* m, const float* base, long long inner, long long outer,
+                   long long row_stride, int nchunk) {
+  cuuint64_t dims[3] = {32, (cuuint64_t)outer, (cuuint64_t)(inner / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)(std::max<long long>(row_stride, inner) * 4), 128};
+  cuuint32_t box[3] = {32, 32, (cuuint32_t)nchunk};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed (" + std::to_string(int(r)) + ")");
 }
 
 struct Role {
@@ -380,12 +617,29 @@ struct Role {
 };
 
 unsigned g_dbg_lbo = 0, g_dbg_sbo = 0;
+bool g_no_tma_store = false;
+int g_prefetch = -1;  // -1: default (off)
+int g_stages = 0;     // 0: as many as fit
+int g_sleep = 1;      // epilogue waits with nanosleep back-off
+bool g_no_3d = false;
+
+inline bool epi_needs_other_host(int op) { return op >= EPI_ADD; }
+
+struct SchedCol { int prob, tq, tp0, ntp, kb; };
+struct SchedPiece { int group, kb0, kb1; };
 
 }  // namespace
 
 void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   g_dbg_lbo = lbo;
   g_dbg_sbo = sbo;
+  // debug switches: (1,1) direct epilogue stores/loads; (2, n) L2 prefetch distance n-1
+  if (lbo == 1) g_no_tma_store = (sbo == 1);
+  if (lbo == 2) g_prefetch = int(sbo) - 1;
+  if (lbo == 4) g_stages = int(sbo);
+  if (lbo == 5) g_sleep = (sbo != 2);  // (5,2) spin without back-off
+  if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
+  if (lbo >= 1 && lbo <= 5) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
 bool gemm_view_ok(const MatView& v) {
@@ -393,6 +647,114 @@ bool gemm_view_ok(const MatView& v) {
   if ((reinterpret_cast<uintptr_t>(v.ptr) & 15) != 0) return false;
   if (v.rows > 1 && (v.rs % 4) != 0) return false;
   return true;
+}
+
+// Host tile scheduler.  A "column" is G P-tiles sharing one Q-tile of one problem; a group of
+// G CTAs walks columns with CTA j of the group on P-tile (column base + j).  Units of work are
+// (column, k-block); each group gets a contiguous, equal share of the units (stream-K) or, when
+// there are plenty of columns, a contiguous run of whole columns.
+GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int num_sms,
+                           int force_groups) {
+  GemmSchedule S;
+  if (probs.empty()) return S;
+  // group width: the P-tile count of small-M problems whose Q operand is large (streamed)
+  int G = 1;
+  bool same_tp = true;
+  for (const auto& pr : probs) same_tp = same_tp && pr.tiles_p == probs[0].tiles_p;
+  const double q_bytes = 4.0 * double(probs[0].Q) * double(probs[0].K);
+  if (same_tp && probs[0].tiles_p >= 2 && probs[0].tiles_p <= 8 && 2 * probs[0].tiles_p <= num_sms &&
+      q_bytes > 32.0 * (1 << 20))
+    G = probs[0].tiles_p;
+  std::vector<SchedCol> cols;
+  for (int pi = 0; pi < int(probs.size()); ++pi) {
+    const GemmProblem& pr = probs[size_t(pi)];
+    for (int tq = 0; tq < pr.tiles_q; ++tq)
+      for (int tp0 = 0; tp0 < pr.tiles_p; tp0 += G)
+        cols.push_back({pi, tq, tp0, std::min(G, pr.tiles_p - tp0), pr.kb_total});
+  }
+  long long U = 0;
+  for (const auto& c : cols) U += c.kb;
+  int groups = std::max(1, num_sms / G);
+  // at least ~8 k-blocks per group so a partial tile amortises its workspace round trip
+  groups = int(std::min<long long>(groups, std::max<long long>(1, U / 8)));
+  if (force_groups > 0) groups = force_groups;
+  const int ncols = int(cols.size());
+  const bool whole = ncols >= 8 * groups || ncols % groups == 0;
+  if (whole) groups = std::min(groups, ncols);
+
+  // pieces[col] = ordered (group, kb0, kb1)
+  std::vector<std::vector<SchedPiece>> pieces(static_cast<size_t>(ncols));
+  std::vector<std::vector<std::pair<int, int>>> group_pieces(static_cast<size_t>(groups));  // (col, piece idx)
+  if (whole) {
+    for (int g = 0; g < groups; ++g) {
+      const int c0 = int((long long)ncols * g / groups), c1 = int((long long)ncols * (g + 1) / groups);
+      for (int c = c0; c < c1; ++c) {
+        pieces[size_t(c)].push_back({g, 0, cols[size_t(c)].kb});
+        group_pieces[size_t(g)].push_back({c, 0});
+      }
+    }
+  } else {
+    long long col_start = 0;
+    int c = 0;
+    for (int g = 0; g < groups; ++g) {
+      const long long u0 = U * g / groups, u1 = U * (g + 1) / groups;
+      long long u = u0;
+      while (u < u1) {
+        while (u >= col_start + cols[size_t(c)].kb) col_start += cols[size_t(c++)].kb;
+        const long long end = std::min(u1, col_start + cols[size_t(c)].kb);
+        pieces[size_t(c)].push_back({g, int(u - col_start), int(end - col_start)});
+        group_pieces[size_t(g)].push_back({c, int(pieces[size_t(c)].size()) - 1});
+        u = end;
+      }
+    }
+  }
+  // slots: one per non-head piece per P-tile lane
+  std::vector<int> slot_base(size_t(ncols) * size_t(G), -1);
+  int nslots = 0;
+  for (int c = 0; c < ncols; ++c) {
+    const int np = int(pieces[size_t(c)].size());
+    if (np <= 1) continue;
+    for (int j = 0; j < cols[size_t(c)].ntp; ++j) {
+      slot_base[size_t(c) * G + j] = nslots;
+      nslots += np - 1;
+    }
+  }
+  S.grid = groups * G;
+  S.seg_off.assign(size_t(S.grid) + 1, 0);
+  for (int g = 0; g < groups; ++g) {
+    for (int j = 0; j < G; ++j) {
+      const int cta = g * G + j;
+      for (const auto& cp : group_pieces[size_t(g)]) {
+        const SchedCol& col = cols[size_t(cp.first)];
+        if (j >= col.ntp) continue;
+        const auto& ps = pieces[size_t(cp.first)];
+        const SchedPiece& pc = ps[size_t(cp.second)];
+        GemmSeg sg;
+        sg.prob = col.prob;
+        sg.tp = col.tp0 + j;
+        sg.tq = col.tq;
+        sg.kb0 = pc.kb0;
+        sg.kb1 = pc.kb1;
+        if (ps.size() == 1) {
+          sg.kind = SEG_WHOLE;
+        } else if (cp.second == 0) {
+          sg.kind = SEG_HEAD;
+          sg.slot = slot_base[size_t(cp.first) * G + j];
+          sg.n_parts = int(ps.size()) - 1;
+        } else {
+          sg.kind = SEG_PART;
+          sg.slot = slot_base[size_t(cp.first) * G + j] + cp.second - 1;
+        }
+        S.segs.push_back(sg);
+      }
+      S.seg_off[size_t(cta) + 1] = int(S.segs.size());
+    }
+  }
+  S.nslots = nslots;
+  S.group = G;
+  S.stream_k = !whole;
+  (void)bn;
+  return S;
 }
 
 GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool split) {
@@ -408,9 +770,10 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   g.nprob = int(specs.size());
 
   std::vector<CUtensorMap> maps(2 * specs.size());
+  std::vector<CUtensorMap> store_maps;  // epilogue operand maps
+  std::vector<std::pair<int, int>> store_idx;  // (problem, output index)
   std::vector<GemmProblem>& probs = g.host_problems;
   probs.resize(specs.size());
-  long long total_tiles = 0;
   for (size_t i = 0; i < specs.size(); ++i) {
     const GemmSpec& s = specs[i];
     if (!gemm_view_ok(s.a) || !gemm_view_ok(s.b))
@@ -430,9 +793,19 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     } else if (g.p_mn != rp.mn || g.q_mn != rq.mn) {
       throw std::runtime_error("gemm: mixed operand majorness in one batch");
     }
-    make_map(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, 32, rp.mn ? 32 : BM, rp.mn);
-    make_map(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, 32, rq.mn ? 32 : g.bn, rq.mn);
     GemmProblem& pr = probs[i];
+    if (rp.mn && rp.inner % 32 == 0 && !g_no_3d) {
+      make_map_mn3d(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, BM / 32);
+      pr.a3d = 1;
+    } else {
+      make_map(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, 32, rp.mn ? 32 : BM, rp.mn);
+    }
+    if (rq.mn && rq.inner % 32 == 0 && !g_no_3d) {
+      make_map_mn3d(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, g.bn / 32);
+      pr.b3d = 1;
+    } else {
+      make_map(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, 32, rq.mn ? 32 : g.bn, rq.mn);
+    }
     pr.P = int(g.swap ? N : M);
     pr.Q = int(g.swap ? M : N);
     pr.K = int(K);
@@ -452,73 +825,90 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
         std::swap(pr.epi[e].out_rs, pr.epi[e].out_cs);
       }
     }
-    total_tiles += (long long)pr.tiles_p * pr.tiles_q;
+    // TMA load map for the epilogue operand (row-major, 16-byte aligned base and pitch)
+    auto storable = [&](const float* b, long long rs, long long cs) {
+      return b && cs == 1 && (reinterpret_cast<uintptr_t>(b) & 15) == 0 && (pr.P == 1 || rs % 4 == 0);
+    };
+    for (int e = 0; e < s.n_epi; ++e) {
+      if (!epi_needs_other_host(pr.epi[e].op)) continue;
+      pr.other_stage = e;
+      if (!g_no_tma_store && storable(pr.epi[e].other, pr.epi[e].o_rs, pr.epi[e].o_cs)) {
+        store_maps.emplace_back();
+        make_map(&store_maps.back(), pr.epi[e].other, pr.Q, pr.P, pr.epi[e].o_rs, CW, 32, false, true);
+        store_idx.push_back({int(i), 1 + kMaxEpi});
+        g.other_smem = true;
+      }
+      break;
+    }
+    auto small = [](long long x) { return x >= 0 && x < (1ll << 31); };
+    bool ok = small(pr.out_rs) && small(pr.out_cs);
+    for (int e = 0; e < s.n_epi; ++e) ok = ok && small(pr.epi[e].out_rs) && small(pr.epi[e].out_cs);
+    if (!ok) throw std::runtime_error("gemm: output strides exceed 2^31 elements");
     g.flops += 2.0 * double(M) * double(N) * double(K);
     g.min_bytes += 4.0 * double(M * K + K * N + M * N * (1 + s.n_epi));
     for (int e = 0; e < s.n_epi; ++e)
       if (s.epi[e].op >= EPI_ADD) g.min_bytes += 4.0 * double(M * N);
   }
-  // K-split: minimise waves of work per unit of work, favouring fewer splits.
-  const int kb = probs[0].kb_total;
-  int best_s = 1;
-  double best_cost = 1e30;
-  for (int s = 1; s <= 32; ++s) {
-    if (s > 1 && kb / s < 8) break;
-    const long long units = total_tiles * s;
-    const double waves = double((units + num_sms - 1) / num_sms);
-    const double cost = waves / s * (1.0 + 0.01 * s);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best_s = s;
+  // L2 policy: operands re-read by many tiles and small enough to stay resident are kept
+  // (evict_last); large streamed ones (a weight read once per step) and epilogue outputs far
+  // larger than L2 are evict_first, so they do not push the reused operands out.
+  {
+    double pb = 0, qb = 0, ob = 0;
+    for (size_t i = 0; i < probs.size(); ++i) {
+      pb += 4.0 * probs[i].P * double(probs[i].K);
+      qb += 4.0 * probs[i].Q * double(probs[i].K);
+      ob += 4.0 * probs[i].P * double(probs[i].Q) * (1 + probs[i].n_epi);
+    }
+    const double kStream = 48.0 * (1 << 20), kOutStream = 64.0 * (1 << 20);
+    for (auto& pr : probs) {
+      pr.a_stream = pb > kStream;
+      pr.b_stream = qb > kStream;
+      pr.out_stream = ob > kOutStream;
     }
   }
-  int unit = 0;
-  size_t ws = 0, cnt = 0;
-  for (auto& pr : probs) {
-    const int kbps = (pr.kb_total + best_s - 1) / best_s;
-    pr.kb_per_split = kbps;
-    pr.splits = (pr.kb_total + kbps - 1) / kbps;
-    pr.unit_begin = unit;
-    unit += pr.tiles_p * pr.tiles_q * pr.splits;
-    if (pr.splits > 1) {
-      ws += size_t(pr.tiles_p) * pr.tiles_q * pr.splits * BM * g.bn;
-      cnt += size_t(pr.tiles_p) * pr.tiles_q;
-    }
+  g.sched = gemm_schedule(probs, g.bn, num_sms, 0);
+  g.units = g.sched.grid;
+  g.ws_floats = size_t(g.sched.nslots) * BM * g.bn;
+  if (g.sched.nslots) {
+    CUDA_CHECK(cudaMalloc(&g.d_ws, g.ws_floats * sizeof(float)));
+    CUDA_CHECK(cudaMalloc(&g.d_flags, size_t(g.sched.nslots) * sizeof(unsigned)));
+    CUDA_CHECK(cudaMemset(g.d_flags, 0, size_t(g.sched.nslots) * sizeof(unsigned)));
   }
-  g.units = unit;
-  g.ws_floats = ws;
-  g.n_counters = cnt;
-  if (ws) {
-    CUDA_CHECK(cudaMalloc(&g.d_ws, ws * sizeof(float)));
-    CUDA_CHECK(cudaMalloc(&g.d_counters, cnt * sizeof(unsigned)));
-    CUDA_CHECK(cudaMemset(g.d_counters, 0, cnt * sizeof(unsigned)));
-  }
-  size_t wo = 0, co = 0;
-  for (auto& pr : probs) {
-    if (pr.splits > 1) {
-      pr.ws = g.d_ws + wo;
-      pr.counters = g.d_counters + co;
-      wo += size_t(pr.tiles_p) * pr.tiles_q * pr.splits * BM * g.bn;
-      co += size_t(pr.tiles_p) * pr.tiles_q;
-    }
-  }
+  const size_t nload = maps.size();
+  maps.insert(maps.end(), store_maps.begin(), store_maps.end());
   CUDA_CHECK(cudaMalloc(&g.d_tmaps, maps.size() * sizeof(CUtensorMap)));
   CUDA_CHECK(cudaMemcpy(g.d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   for (size_t i = 0; i < probs.size(); ++i) {
     probs[i].tmap_a = static_cast<CUtensorMap*>(g.d_tmaps) + 2 * i;
     probs[i].tmap_b = static_cast<CUtensorMap*>(g.d_tmaps) + 2 * i + 1;
   }
+  for (size_t j = 0; j < store_idx.size(); ++j) {
+    GemmProblem& pr = probs[size_t(store_idx[j].first)];
+    const void* m = static_cast<CUtensorMap*>(g.d_tmaps) + nload + j;
+    pr.tmap_other = m;
+  }
   CUDA_CHECK(cudaMalloc(&g.d_problems, probs.size() * sizeof(GemmProblem)));
   CUDA_CHECK(cudaMemcpy(g.d_problems, probs.data(), probs.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
-  g.smem_bytes = smem_for(g.bn, split);
+  CUDA_CHECK(cudaMalloc(&g.d_segs, g.sched.segs.size() * sizeof(GemmSeg) + 16));
+  CUDA_CHECK(cudaMemcpy(g.d_segs, g.sched.segs.data(), g.sched.segs.size() * sizeof(GemmSeg), cudaMemcpyHostToDevice));
+  CUDA_CHECK(cudaMalloc(&g.d_seg_off, g.sched.seg_off.size() * sizeof(int)));
+  CUDA_CHECK(cudaMemcpy(g.d_seg_off, g.sched.seg_off.data(), g.sched.seg_off.size() * sizeof(int), cudaMemcpyHostToDevice));
+  g.stages = stages_for(g.bn, split, g.other_smem);
+  if (g_stages > 0) g.stages = std::min(g.stages, g_stages);
+  g.smem_bytes = smem_for(g.bn, split, g.other_smem, g.stages);
+  g.prefetch = g_prefetch >= 0 ? g_prefetch : 0;
+  g.threads = threads_for(split);
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, split);
-  CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(g.smem_bytes)));
+  // the attribute is per function and launches of one instantiation differ in smem: allow the max
+  CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)));
   return g;
 }
 
 void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split);
-  fn<<<g.units, 256, g.smem_bytes, stream>>>(static_cast<const GemmProblem*>(g.d_problems), g.nprob);
+  fn<<<g.sched.grid, g.threads, g.smem_bytes, stream>>>(
+      static_cast<const GemmProblem*>(g.d_problems), static_cast<const GemmSeg*>(g.d_segs),
+      g.d_seg_off, g.d_ws, g.d_flags, g.stages, g.prefetch, (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0));
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -526,7 +916,9 @@ void gemm_free(GemmLaunch& g) {
   if (g.d_problems) cudaFree(g.d_problems);
   if (g.d_tmaps) cudaFree(g.d_tmaps);
   if (g.d_ws) cudaFree(g.d_ws);
-  if (g.d_counters) cudaFree(g.d_counters);
+  if (g.d_flags) cudaFree(g.d_flags);
+  if (g.d_segs) cudaFree(g.d_segs);
+  if (g.d_seg_off) cudaFree(g.d_seg_off);
   g = GemmLaunch{};
 }
 

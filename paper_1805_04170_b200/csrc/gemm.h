@@ -40,15 +40,38 @@ struct GemmProblem {
   const void* tmap_a = nullptr;  // P operand
   const void* tmap_b = nullptr;  // Q operand
   int P = 0, Q = 0, K = 0;
-  int tiles_p = 0, tiles_q = 0, splits = 1, kb_per_split = 0, kb_total = 0;
-  int unit_begin = 0;
+  int tiles_p = 0, tiles_q = 0, kb_total = 0;
   float* out = nullptr;
   long long out_rs = 0, out_cs = 0;
   int n_epi = 0;
   EpiStage epi[kMaxEpi];
   unsigned mn_lbo = 4096, mn_sbo = 512;  // MN-major (128B_BASE32B) descriptor strides (bytes)
-  float* ws = nullptr;          // split-K partial tiles
-  unsigned int* counters = nullptr;
+  // MN-major operand mapped in 3-D (32-wide chunk, K, chunk index): one TMA op per k-block
+  int a3d = 0, b3d = 0;
+  // L2 policy per operand (0 = evict_last: small and re-read by many tiles; 1 = evict_first:
+  // streamed) and streaming (.cs) epilogue stores for outputs far larger than L2
+  int a_stream = 0, b_stream = 0, out_stream = 0;
+  // TMA load map of the first epilogue stage's second operand (same 32 x 32 boxes), or null.
+  const void* tmap_other = nullptr;
+  int other_stage = -1;         // which epi stage tmap_other feeds
+};
+
+// One unit of a CTA's work list: k-blocks [kb0, kb1) of output tile (tp, tq) of problem `prob`.
+// kind 0 = the whole k range (epilogue, no partials); 1 = head of a cut tile (waits for
+// n_parts partial slots starting at `slot`, sums them in k order, runs the epilogue);
+// 2 = a later k range of a cut tile (writes partial slot `slot` and raises its flag).
+struct GemmSeg {
+  int prob = 0, tp = 0, tq = 0, kb0 = 0, kb1 = 0;
+  int kind = 0, slot = 0, n_parts = 0;
+};
+
+struct GemmSchedule {
+  int grid = 0;                 // persistent CTAs (<= SM count)
+  int group = 1;                // CTAs walking the same k ranges on neighbouring P-tiles
+  bool stream_k = false;
+  int nslots = 0;               // partial-tile workspace slots
+  std::vector<GemmSeg> segs;    // all CTAs' lists, concatenated
+  std::vector<int> seg_off;     // CTA c owns segs[seg_off[c], seg_off[c+1])
 };
 
 // Host-side description of one sub-op matmul over strided row-major fp32 views.
@@ -71,13 +94,20 @@ struct GemmLaunch {
   int bn = 0;
   bool split = false;           // 3xTF32
   bool p_mn = false, q_mn = false, swap = false;
-  int units = 0;
+  int units = 0;                // CTAs launched
   int nprob = 0;
+  int threads = 256;
+  int stages = 0;               // smem ring depth
+  int prefetch = 0;             // k-blocks of L2 prefetch ahead of the ring (0 = off)
+  bool other_smem = false;      // epilogue operand staged through TMA
+  GemmSchedule sched;
   void* d_problems = nullptr;   // GemmProblem[nprob] on device
   void* d_tmaps = nullptr;      // 2*nprob CUtensorMap on device
-  float* d_ws = nullptr;
-  unsigned int* d_counters = nullptr;
-  size_t ws_floats = 0, n_counters = 0;
+  void* d_segs = nullptr;       // GemmSeg[] on device
+  int* d_seg_off = nullptr;
+  float* d_ws = nullptr;        // partial tiles (stream-K)
+  unsigned int* d_flags = nullptr;
+  size_t ws_floats = 0;
   size_t smem_bytes = 0;
   std::vector<GemmProblem> host_problems;  // for inspection (roofline accounting)
   double flops = 0;             // 2*M*N*K summed
@@ -92,6 +122,9 @@ bool gemm_view_ok(const MatView& v);
 // split = 3xTF32 (fp32-accurate products), else single-pass TF32.
 GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool split = false);
 void gemm_run(const GemmLaunch& g, cudaStream_t stream);
+// The tile scheduler alone (host only; exposed for tests).  force_groups > 0 overrides the
+// group count.
+GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int num_sms, int force_groups);
 void gemm_free(GemmLaunch& g);
 // Debug override of the MN-major descriptor strides (0 = defaults).
 void gemm_debug_mn_desc(unsigned lbo, unsigned sbo);

@@ -861,7 +861,8 @@ std::string describe(const PlanRt& P) {
         if (size_t(st.idx) < prog.gemm.size()) {
           const GemmLaunch& gl = prog.gemm[size_t(st.idx)];
           s << ",\"bn\":" << gl.bn << ",\"swap\":" << gl.swap << ",\"units\":" << gl.units
-            << ",\"splits\":" << (gl.host_problems.empty() ? 1 : gl.host_problems[0].splits);
+            << ",\"stream_k\":" << gl.sched.stream_k << ",\"group\":" << gl.sched.group
+            << ",\"segments\":" << gl.sched.segs.size() << ",\"partial_slots\":" << gl.sched.nslots;
         }
       } else if (st.kind == ST_XCHG) {
         const XchgGroup& g = prog.xchg[size_t(st.idx)];

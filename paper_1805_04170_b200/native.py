@@ -63,6 +63,12 @@ _SIGS = {
     "tpx_gemm": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_i64,
                  c_int, P(c_int), P(ctypes.c_float), P(c_vp), P(c_i64), P(c_vp), P(c_i64), c_int,
                  c_u64],
+    "tpx_gemm_timed": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp,
+                       c_i64, c_int, P(c_int), P(ctypes.c_float), P(c_vp), P(c_i64), P(c_vp),
+                       P(c_i64), c_int, c_u64, c_int, c_int, P(c_dbl)],
+    "tpx_gemm_schedule": [c_int, c_int, c_int, c_int, c_int, c_int, c_int, P(c_int), P(c_int),
+                          P(c_int), P(c_int), P(c_int), P(ctypes.c_int32), c_int,
+                          P(ctypes.c_int32), c_int],
     "tpx_debug_gemm_mn_desc": [ctypes.c_uint, ctypes.c_uint],
 }
 
@@ -101,9 +107,12 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None, precision: int = 0):
+def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None, precision: int = 0,
+         warmup: int = 0, iters: int = 0):
     """C = op(A) @ op(B) on the tcgen05 path; A, B, C are 2-D fp32 CUDA tensors with unit
-    inner stride.  `epi` = [(op, scale, other_or_None, out), ...] (gemm.h EpiOp codes)."""
+    inner stride.  `epi` = [(op, scale, other_or_None, out), ...] (gemm.h EpiOp codes).
+    With iters > 0 the prepared launch runs `warmup` + `iters` times and the mean device time
+    (ms, CUDA events on the stream) is returned."""
     import torch  # plumbing only: device pointers and the current stream
 
     for t in (A, B, C):
@@ -118,6 +127,29 @@ def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None, precision: int = 0)
     outs = (c_vp * max(n, 1))(*[e[3].data_ptr() for e in epi])
     outs_rs = (c_i64 * max(n, 1))(*[e[3].stride(0) for e in epi])
     s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-    check(lib().tpx_gemm(_ptr(A), A.shape[0], A.shape[1], A.stride(0), _ptr(B), B.shape[0],
-                         B.shape[1], B.stride(0), int(ta), int(tb), _ptr(C), C.stride(0), n, ops,
-                         scales, others, others_rs, outs, outs_rs, int(precision), s))
+    ms = c_dbl(0.0)
+    check(lib().tpx_gemm_timed(_ptr(A), A.shape[0], A.shape[1], A.stride(0), _ptr(B), B.shape[0],
+                               B.shape[1], B.stride(0), int(ta), int(tb), _ptr(C), C.stride(0), n,
+                               ops, scales, others, others_rs, outs, outs_rs, int(precision), s,
+                               int(warmup), int(iters), ctypes.byref(ms)))
+    return ms.value if iters > 0 else None
+
+
+def gemm_schedule(nprob: int, P_: int, Q: int, K: int, bn: int, num_sms: int = 148,
+                  force_groups: int = 0):
+    """Host-only view of the persistent GEMM's tile schedule (gemm.cu gemm_schedule):
+    returns dict(grid, group, stream_k, nslots, segs=[(prob,tp,tq,kb0,kb1,kind,slot,n_parts)],
+    seg_off=[...])."""
+    grid, nsegs, nslots, group, sk = (c_int(), c_int(), c_int(), c_int(), c_int())
+    check(lib().tpx_gemm_schedule(nprob, P_, Q, K, bn, num_sms, force_groups, ctypes.byref(grid),
+                                  ctypes.byref(nsegs), ctypes.byref(nslots), ctypes.byref(group),
+                                  ctypes.byref(sk), None, 0, None, 0))
+    segs = (ctypes.c_int32 * (8 * max(nsegs.value, 1)))()
+    off = (ctypes.c_int32 * (grid.value + 1))()
+    check(lib().tpx_gemm_schedule(nprob, P_, Q, K, bn, num_sms, force_groups, ctypes.byref(grid),
+                                  ctypes.byref(nsegs), ctypes.byref(nslots), ctypes.byref(group),
+                                  ctypes.byref(sk), segs, nsegs.value, off, grid.value))
+    return {"grid": grid.value, "group": group.value, "stream_k": bool(sk.value),
+            "nslots": nslots.value,
+            "segs": [tuple(segs[8 * i: 8 * i + 8]) for i in range(nsegs.value)],
+            "seg_off": list(off)}
