@@ -39,7 +39,8 @@ constexpr int BK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
 constexpr int CW = 16;                                    // epilogue chunk: 16 accumulator columns
 constexpr uint32_t kOutStage = 32 * CW * 4;               // one 32-row x CW fp32 box (64B swizzle)
 constexpr uint32_t kOutStageBytes = 8 * kOutStage;        // <= 8 epilogue warps x 1 transpose box
-constexpr uint32_t kOtherBytes = 8 * kOutStage;           // <= 8 epilogue warps x 1 operand box
+constexpr int kOtherDepth = 4;                            // max operand boxes in flight per warp
+constexpr uint32_t kOtherBox = 8 * kOutStage;             // one box for each of <= 8 epilogue warps
 constexpr uint32_t kSmemMax = 232448;                     // 227 KB opt-in
 constexpr uint32_t kBarBytes = 512;
 
@@ -49,12 +50,13 @@ __host__ __device__ constexpr uint32_t operand_bytes(int bn) { return uint32_t(B
 __host__ __device__ constexpr uint32_t stage_bytes(int bn, bool split) {
   return operand_bytes(bn) * (split ? 2u : 1u);
 }
-inline int stages_for(int bn, bool split, bool other) {
-  const uint32_t budget = kSmemMax - 1024 - kBarBytes - kOutStageBytes - (other ? kOtherBytes : 0);
+// odepth = operand boxes in flight per epilogue warp (0 = no TMA-staged operand)
+inline int stages_for(int bn, bool split, int odepth) {
+  const uint32_t budget = kSmemMax - 1024 - kBarBytes - kOutStageBytes - odepth * kOtherBox;
   return std::min<int>(8, int(budget / stage_bytes(bn, split)));
 }
-inline size_t smem_for(int bn, bool split, bool other, int stages) {
-  return size_t(stages) * stage_bytes(bn, split) + kOutStageBytes + (other ? kOtherBytes : 0) + 1024 + kBarBytes;
+inline size_t smem_for(int bn, bool split, int odepth, int stages) {
+  return size_t(stages) * stage_bytes(bn, split) + kOutStageBytes + odepth * kOtherBox + 1024 + kBarBytes;
 }
 // 12 warps: producer, MMA, TMEM allocator, spare, then 8 epilogue warps (two per TMEM lane
 // quarter, each on half the tile's columns) -- or, for 3xTF32, 4 epilogue + 4 splitting warps.
@@ -190,6 +192,51 @@ __device__ __forceinline__ void store_block(uint32_t sbuf, int lane, const float
   __syncwarp();
 }
 
+// Elementwise stage on 4 values (store-order epilogue).
+__device__ __forceinline__ float epi1(int op, float v, float o, float s) {
+  switch (op) {
+    case EPI_TANH: return tanhf(v);
+    case EPI_DTANH: { const float t = tanhf(v); return 1.0f - t * t; }
+    case EPI_SCALE: return s * v;
+    case EPI_ADD: return v + o;
+    case EPI_SUB_PO: return v - o;
+    case EPI_SUB_OP: return o - v;
+    default: return v;
+  }
+}
+__device__ __forceinline__ void epi_apply4(int op, float4 (&x)[4], const float4 (&o)[4], float s) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[i].x = epi1(op, x[i].x, o[i].x, s);
+    x[i].y = epi1(op, x[i].y, o[i].y, s);
+    x[i].z = epi1(op, x[i].z, o[i].z, s);
+    x[i].w = epi1(op, x[i].w, o[i].w, s);
+  }
+}
+// Store-order block store: x[i] = row (i*8 + lane/4), columns q0 + 4*(lane%4) .. +3 of a warp's
+// 32 x CW block; each instruction writes 8 rows x 64 contiguous bytes.
+__device__ __forceinline__ void store_block_so(const float4 (&x)[4], int lane, float* base, long long rs,
+                                               int prow0, int q0, int P, int Q, bool stream) {
+  const int gq = q0 + (lane & 3) * 4;
+  const bool vec = ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && ((rs & 3) == 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gp = prow0 + i * 8 + (lane >> 2);
+    if (gp < P) {
+      float* dst = base + (long long)gp * rs + gq;
+      if (vec && gq + 4 <= Q) {
+        if (stream) __stcs(reinterpret_cast<float4*>(dst), x[i]);
+        else *reinterpret_cast<float4*>(dst) = x[i];
+      } else {
+        if (gq < Q) dst[0] = x[i].x;
+        if (gq + 1 < Q) dst[1] = x[i].y;
+        if (gq + 2 < Q) dst[2] = x[i].z;
+        if (gq + 3 < Q) dst[3] = x[i].w;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void flag_release(unsigned* f) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(1u) : "memory");
 }
@@ -199,8 +246,9 @@ __device__ __forceinline__ unsigned flag_acquire(const unsigned* f) {
   return v;
 }
 
-// Partial tiles live in L2-resident workspace slots of BM x BN floats, interleaved so that one
-// warp-wide float4 access (32 rows, same 4 columns) is 512 contiguous bytes.
+// Partial tiles live in L2-resident workspace slots of BM x BN floats (one per CTA; a pair tile
+// has two), interleaved so that one warp-wide float4 access (32 rows, same 4 columns) is 512
+// contiguous bytes.
 __device__ __forceinline__ float4* ws_ptr(float* ws, int slot, int bn, int c0, int j, int row) {
   return reinterpret_cast<float4*>(ws + (size_t)slot * BM * bn) + ((c0 / CW) * (CW / 4) + j) * BM + row;
 }
@@ -208,36 +256,45 @@ __device__ __forceinline__ float4* ws_ptr(float* ws, int slot, int bn, int c0, i
 // SPLIT = 3xTF32: every fp32 operand x = hi + lo with hi = tf32_rna(x), lo = x - hi (exact);
 // D += lo_A*hi_B + hi_A*lo_B + hi_A*hi_B.  The split runs in shared memory between the TMA
 // landing and the MMA issue (warps 8..11).
-template <int BN, bool P_MN, bool Q_MN, bool SPLIT>
+// PAIR = CTA pair (cluster of 2, tcgen05 cta_group::2): one 256 x BN tile per pair; each CTA
+// stages its 128 rows of A and BN/2 columns of B (half the operand bytes per CTA), the leader
+// issues the M = 256 MMAs, and each CTA drains its own 128 accumulator rows.
+template <int BN, bool P_MN, bool Q_MN, bool SPLIT, bool PAIR>
 __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     gemm_tf32_kernel(const GemmProblem* __restrict__ probs, const GemmSeg* __restrict__ segs,
                      const int* __restrict__ seg_off, float* __restrict__ ws,
                      unsigned* __restrict__ flags, const int STAGES, const int PF,
                      const int has_other) {
+  static_assert(!(PAIR && SPLIT), "3xTF32 runs on single-CTA tiles");
+  constexpr int BNH = PAIR ? BN / 2 : BN;     // B columns staged by this CTA
+  constexpr int PBM = PAIR ? 2 * BM : BM;     // rows of one (pair) tile
   constexpr uint32_t A_BYTES = BM * BK * 4;
-  constexpr uint32_t OPB = operand_bytes(BN);
-  constexpr uint32_t STAGE = stage_bytes(BN, SPLIT);
+  constexpr uint32_t OPB = operand_bytes(BNH);
+  constexpr uint32_t STAGE = stage_bytes(BNH, SPLIT);
   constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
   constexpr int NEPI = epi_warps(SPLIT);
   constexpr uint32_t IDESC = (1u << 4)                 // D format f32
                              | (2u << 7) | (2u << 10)  // A, B format tf32
                              | (uint32_t(P_MN) << 15) | (uint32_t(Q_MN) << 16) |
-                             (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+                             (uint32_t(BN >> 3) << 17) | (uint32_t(PBM >> 4) << 24);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* out_stage = smem + STAGES * STAGE;  // [4 warps][32 rows x 128 B] store transpose
-  uint8_t* other_stage = out_stage + kOutStageBytes;  // [8 warps][32 rows x 64 B] if has_other
-  uint64_t* full = reinterpret_cast<uint64_t*>(other_stage + ((has_other & 1) ? kOtherBytes : 0));
+  uint8_t* other_stage = out_stage + kOutStageBytes;  // [8 warps][depth][32 rows x 64 B] if has_other
+  const int ODEPTH = (has_other >> 4) & 7;  // operand ring depth (0 when unused)
+  uint64_t* full = reinterpret_cast<uint64_t*>(other_stage + ODEPTH * kOtherBox);
   uint64_t* empty = full + STAGES;
   uint64_t* split_done = empty + STAGES;
   uint64_t* tmem_full = split_done + STAGES;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;       // [2]
-  uint64_t* other_bar = tmem_empty + 2;       // [8] one per epilogue warp
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(other_bar + 8);
+  uint64_t* other_bar = tmem_empty + 2;       // [8 warps][depth]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(other_bar + 8 * kOtherDepth);
 
-  const int s_begin = seg_off[blockIdx.x], s_end = seg_off[blockIdx.x + 1];
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;  // 0 = MMA leader of the pair
+  const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int s_begin = seg_off[unit], s_end = seg_off[unit + 1];
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -247,37 +304,53 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], NEPI);  // one arrival per epilogue warp
+      mbar_init(&tmem_empty[a], PAIR ? 2 * NEPI : NEPI);  // one arrival per epilogue warp (of both CTAs)
     }
-    for (int w = 0; w < 8; ++w) mbar_init(&other_bar[w], 1);
+    for (int w = 0; w < 8 * kOtherDepth; ++w) mbar_init(&other_bar[w], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_holder, TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_pair(tmem_holder, TMEM_COLS);
+    else tmem_alloc(tmem_holder, TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the peer's barriers are initialised before any remote use
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // the leader's barriers, as shared::cluster addresses (pair TMA and epilogue arrivals)
+  const uint32_t full_lead = PAIR ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
+  const uint32_t tmem_empty_lead = PAIR ? mapa_shared(smem_u32(tmem_empty), 0) : smem_u32(tmem_empty);
 
   // One k-block of operands: K-major tiles are one 2-D box; MN-major tiles are 32-wide
   // 128B_BASE32B-swizzled chunks 4096 bytes apart, one 3-D box when the extent allows.
+  auto ld2 = [&](void* dst, const void* map, uint64_t* bar, uint32_t bar_c, int c0, int c1, uint64_t pol) {
+    if constexpr (PAIR) tma_load_2d_pair(dst, map, bar_c, c0, c1, pol);
+    else tma_load_2d_hint(dst, map, bar, c0, c1, pol);
+  };
+  auto ld3 = [&](void* dst, const void* map, uint64_t* bar, uint32_t bar_c, int c0, int c1, int c2, uint64_t pol) {
+    if constexpr (PAIR) tma_load_3d_pair(dst, map, bar_c, c0, c1, c2, pol);
+    else tma_load_3d_hint(dst, map, bar, c0, c1, c2, pol);
+  };
+  // bar: local barrier (single CTA); bar_c: the leader's barrier in the cluster window (pair)
   auto load_kblock = [&](const GemmProblem& pr, int kb, int p0, int q0, uint8_t* sa, uint8_t* sb,
-                         uint64_t* bar, uint64_t pol_a, uint64_t pol_b) {
+                         uint64_t* bar, uint32_t bar_c, uint64_t pol_a, uint64_t pol_b) {
     const int k0 = kb * BK;
     if constexpr (!P_MN) {
-      tma_load_2d_hint(sa, pr.tmap_a, bar, k0, p0, pol_a);
+      ld2(sa, pr.tmap_a, bar, bar_c, k0, p0, pol_a);
     } else if (pr.a3d) {
-      tma_load_3d_hint(sa, pr.tmap_a, bar, 0, k0, p0 / 32, pol_a);
+      ld3(sa, pr.tmap_a, bar, bar_c, 0, k0, p0 / 32, pol_a);
     } else {
 #pragma unroll
-      for (int j = 0; j < BM / 32; ++j) tma_load_2d_hint(sa + j * 4096, pr.tmap_a, bar, p0 + 32 * j, k0, pol_a);
+      for (int j = 0; j < BM / 32; ++j) ld2(sa + j * 4096, pr.tmap_a, bar, bar_c, p0 + 32 * j, k0, pol_a);
     }
     if constexpr (!Q_MN) {
-      tma_load_2d_hint(sb, pr.tmap_b, bar, k0, q0, pol_b);
+      ld2(sb, pr.tmap_b, bar, bar_c, k0, q0, pol_b);
     } else if (pr.b3d) {
-      tma_load_3d_hint(sb, pr.tmap_b, bar, 0, k0, q0 / 32, pol_b);
+      ld3(sb, pr.tmap_b, bar, bar_c, 0, k0, q0 / 32, pol_b);
     } else {
 #pragma unroll
-      for (int j = 0; j < BN / 32; ++j) tma_load_2d_hint(sb + j * 4096, pr.tmap_b, bar, q0 + 32 * j, k0, pol_b);
+      for (int j = 0; j < BNH / 32; ++j) ld2(sb + j * 4096, pr.tmap_b, bar, bar_c, q0 + 32 * j, k0, pol_b);
     }
   };
   if (warp == 0 && lane == 0) {
@@ -287,17 +360,18 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     for (int si = s_begin; si < s_end; ++si) {
       const GemmSeg sg = segs[si];
       const GemmProblem& pr = probs[sg.prob];
-      const int p0 = sg.tp * BM, q0 = sg.tq * BN;
+      const int p0 = sg.tp * PBM + int(rank) * BM, q0 = sg.tq * BN + int(rank) * BNH;
       const uint64_t pol_a = pr.a_stream ? stream : keep, pol_b = pr.b_stream ? stream : keep;
       for (int kb = sg.kb0; kb < sg.kb1; ++kb, (++s == uint32_t(STAGES)) ? (s = 0, ph ^= 1) : 0) {
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* sa = smem + s * STAGE;
-        mbar_arrive_expect_tx(&full[s], OPB);
-        load_kblock(pr, kb, p0, q0, sa, sa + A_BYTES, &full[s], pol_a, pol_b);
+        // the leader's full barrier expects both CTAs' bytes; the peer's TMA completes on it
+        if (rank == 0) mbar_arrive_expect_tx(&full[s], PAIR ? 2 * OPB : OPB);
+        load_kblock(pr, kb, p0, q0, sa, sa + A_BYTES, &full[s], full_lead + s * 8, pol_a, pol_b);
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread)
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (single thread; the pair's leader CTA)
     uint32_t s = 0, ph = 0;  // ring slot and its phase parity
     for (int si = s_begin, i = 0; si < s_end; ++si, ++i) {
       const GemmSeg sg = segs[si];
@@ -328,13 +402,17 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             mma_tf32(d, ad + lo, bd, IDESC, accum);
             mma_tf32(d, ad, bd + lo, IDESC, 1u);
             mma_tf32(d, ad, bd, IDESC, 1u);
+          } else if constexpr (PAIR) {
+            mma_tf32_pair(d, ad, bd, IDESC, accum);
           } else {
             mma_tf32(d, ad, bd, IDESC, accum);
           }
         }
-        mma_commit(&empty[s]);
+        if constexpr (PAIR) mma_commit_pair(&empty[s], 0x3);  // frees the slot in both CTAs
+        else mma_commit(&empty[s]);
       }
-      mma_commit(&tmem_full[acc]);
+      if constexpr (PAIR) mma_commit_pair(&tmem_full[acc], 0x3);
+      else mma_commit(&tmem_full[acc]);
     }
   } else if (SPLIT && warp >= 8) {  // (SPLIT: NEPI == 4, epilogue warps 4..7)
     // ---------------- 3xTF32 split: hi in place, lo into the stage's second half
@@ -363,30 +441,47 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     // the columns [ (e/4) BN/2, (e/4+1) BN/2 )
     const int ew = warp - 4;
     const int lq = ew & 3;
-    const int c_begin = NEPI == 8 ? (ew >> 2) * (BN / 2) : 0;
-    const int c_end = NEPI == 8 ? c_begin + BN / 2 : BN;
+    // With 8 warps the two warps of a lane quarter interleave CW-column chunks, so each step
+    // of the pair writes whole 128-byte lines of its rows.
+    const int c_begin = NEPI == 8 ? (ew >> 2) * CW : 0;
+    const int c_end = BN;
+    constexpr int CSTEP = NEPI == 8 ? 2 * CW : CW;
     const int row = lq * 32 + lane;
     const bool leader = (ew == 0 && lane == 0);
-    uint32_t o_used = 0;  // operand boxes consumed by this warp
+    auto wslot = [&](int slot) { return PAIR ? 2 * slot + int(rank) : slot; };  // this CTA's half
+    // Elementwise operand (w for w_next = w - wd): 32 x CW boxes, TMA-loaded ODEPTH chunks
+    // ahead through a per-warp ring.  Lane 0 owns the issue cursor; boxes are issued and
+    // consumed in the same (segment, chunk) order.
+    uint32_t o_slot = 0, o_phase = 0;  // consumer ring position
+    uint32_t i_slot = 0;               // issuer ring position (lane 0)
     const uint64_t o_policy = policy_evict_first();  // the elementwise operand is read once
-    // Request the operand box of the first chunk at or after (si, c0) that consumes one.
-    auto issue_other = [&](int si, int c0) {
-      if (!(has_other & 1)) return;
-      for (; si < s_end; ++si, c0 = c_begin) {
-        const GemmSeg sg = segs[si];
-        if (sg.kind == SEG_PART) continue;
-        const GemmProblem& pr = probs[sg.prob];
-        if (!pr.tmap_other || pr.other_stage < 0) continue;
-        if (c0 < c_end && sg.tq * BN + c0 < pr.Q) {
+    int isi = s_begin, ic0 = c_begin;                 // issue cursor (lane 0)
+    const void* imap = nullptr;
+    int iq = 0, ip = 0, iQ = 0, iseg = -1;
+    auto issue_other = [&]() {
+      for (; isi < s_end; ++isi, ic0 = c_begin) {
+        if (iseg != isi) {
+          const GemmSeg sg = segs[isi];
+          const GemmProblem& pr = probs[sg.prob];
+          iseg = isi;
+          imap = sg.kind == SEG_PART ? nullptr : pr.tmap_other;
+          iq = sg.tq * BN;
+          ip = sg.tp * PBM + int(rank) * BM + lq * 32;
+          iQ = pr.Q;
+        }
+        if (imap && ic0 < c_end && iq + ic0 < iQ) {
+          uint64_t* bar = &other_bar[ew * ODEPTH + i_slot];
           fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&other_bar[ew], kOutStage);
-          tma_load_2d_hint(other_stage + ew * kOutStage, pr.tmap_other, &other_bar[ew], sg.tq * BN + c0,
-                           sg.tp * BM + lq * 32, o_policy);
+          mbar_arrive_expect_tx(bar, kOutStage);
+          tma_load_2d_hint(other_stage + (ew * ODEPTH + i_slot) * kOutStage, imap, bar, iq + ic0, ip, o_policy);
+          if (++i_slot == uint32_t(ODEPTH)) i_slot = 0;
+          ic0 += CSTEP;
           return;
         }
       }
     };
-    if (lane == 0) issue_other(s_begin, c_begin);
+    if ((has_other & 1) && lane == 0)
+      for (int d = 0; d < ODEPTH; ++d) issue_other();
     for (int si = s_begin, i = 0; si < s_end; ++si, ++i) {
       const GemmSeg sg = segs[si];
       const GemmProblem& pr = probs[sg.prob];
@@ -399,7 +494,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
 
       if (sg.kind == SEG_PART) {
 #pragma unroll 1
-        for (int c0 = c_begin; c0 < c_end; c0 += CW) {
+        for (int c0 = c_begin; c0 < c_end; c0 += CSTEP) {
           float v[CW];
           if (have) {
             tmem_ld16(taddr + c0, v);
@@ -409,21 +504,21 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
           }
 #pragma unroll
           for (int j = 0; j < CW / 4; ++j)
-            __stcg(ws_ptr(ws, sg.slot, BN, c0, j, row), make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+            __stcg(ws_ptr(ws, wslot(sg.slot), BN, c0, j, row), make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+        if (lane == 0) mbar_arrive_cluster(tmem_empty_lead + acc * 8);
         __threadfence();
         named_bar_sync(1, NEPI * 32);
-        if (leader) flag_release(&flags[sg.slot]);
+        if (leader) flag_release(&flags[wslot(sg.slot)]);
         continue;
       }
 
       if (sg.kind == SEG_HEAD) {
         if (leader) {
           for (int j = 0; j < sg.n_parts; ++j) {
-            unsigned* f = &flags[sg.slot + j];
+            unsigned* f = &flags[wslot(sg.slot + j)];
             long long t0 = clock64();
             uint32_t spins = 0;
             while (flag_acquire(f) == 0u) {
@@ -436,8 +531,8 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         named_bar_sync(1, NEPI * 32);
       }
 
-      const int p = sg.tp * BM + row;
-      const int prow0 = sg.tp * BM + lq * 32;
+      const int p = sg.tp * PBM + int(rank) * BM + row;
+      const int prow0 = sg.tp * PBM + int(rank) * BM + lq * 32;
       // needs-other stage (w_next = w - wd): its operand is fetched before the TMEM drain
       const int oe = pr.other_stage;
       const void* omap = pr.tmap_other;
@@ -462,31 +557,174 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       }
       const int PP = pr.P, QQ = pr.Q;
       const bool ostream = pr.out_stream != 0;
+      // Store-order fast path: every output row-major and the only second operand TMA-staged.
+      // The accumulator chunk is transposed once through smem and the whole elementwise chain
+      // runs on the transposed values (the operand box already has that layout).
+      bool fast = oe < 0 || o_tma;
+#pragma unroll
+      for (int e = 0; e <= kMaxEpi; ++e)
+        if (e < nout) {
+          fast = fast && ocs[e] == 1;
+          if (e > 0 && epi_needs_other(eop[e - 1]) && e - 1 != oe) fast = false;
+        }
+      if (fast) {
+        // Per-segment store state: row pointer of row (prow0 + lane/4), column 4*(lane%4), per
+        // output, and the 8-row step.  The elementwise chain is matched against the fused
+        // patterns the lowering emits (act, dact, act+seed, step+upd) so the hot loop is
+        // straight-line code.
+        const int c = lane & 3;
+        float* dp[1 + kMaxEpi];
+        long long st8[1 + kMaxEpi];
+        bool vec_ok = true;
+#pragma unroll
+        for (int e = 0; e <= kMaxEpi; ++e) {
+          dp[e] = nullptr;
+          st8[e] = 0;
+          if (e < nout) {
+            vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(obase[e]) & 15) == 0) && ((ors[e] & 3) == 0);
+            dp[e] = obase[e] + (long long)(prow0 + (lane >> 2)) * ors[e] + c * 4;
+            st8[e] = 8ll * ors[e];
+          }
+        }
+        const bool rows_in = prow0 + 32 <= PP;
+        const int n_epi = nout - 1;
+        int chain = 5;  // generic
+        if (n_epi == 0) chain = 0;
+        else if (n_epi == 1 && eop[0] == EPI_TANH) chain = 1;
+        else if (n_epi == 1 && eop[0] == EPI_DTANH) chain = 2;
+        else if (n_epi == 2 && eop[0] == EPI_SCALE && eop[1] == EPI_SUB_OP && oe == 1) chain = 3;
+        else if (n_epi == 2 && eop[0] == EPI_TANH && eop[1] == EPI_DTANH) chain = 4;
+        const float s0 = esc[0];
 #pragma unroll 1
-      for (int c0 = c_begin; c0 < c_end; c0 += CW) {
+        for (int c0 = c_begin; c0 < c_end; c0 += CSTEP) {
+          const int q0 = sg.tq * BN + c0;
+          float v[CW];
+          if (have) {
+            tmem_ld16(taddr + c0, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) v[j] = 0.f;
+          }
+          if (c0 + CSTEP >= c_end) {
+            // accumulator drained: hand it back to the MMA warp before the global traffic
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tmem_empty_lead + acc * 8);
+          }
+          if (q0 >= QQ) continue;
+          if (sg.kind == SEG_HEAD) {
+            for (int pp = 0; pp < sg.n_parts; ++pp) {
+#pragma unroll
+              for (int j = 0; j < CW / 4; ++j) {
+                const float4 x = __ldcg(ws_ptr(ws, wslot(sg.slot + pp), BN, c0, j, row));
+                v[4 * j] += x.x; v[4 * j + 1] += x.y; v[4 * j + 2] += x.z; v[4 * j + 3] += x.w;
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < CW / 4; ++j) sts128(sbuf + box_off(lane, j), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          __syncwarp();
+          float4 x[4], ox[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) x[i] = lds128(sbuf + box_off(i * 8 + (lane >> 2), c));
+          if (oe >= 0) {
+            mbar_wait(&other_bar[ew * ODEPTH + o_slot], o_phase);
+            const uint32_t ob = smem_u32(other_stage + (ew * ODEPTH + o_slot) * kOutStage);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ox[i] = lds128(ob + box_off(i * 8 + (lane >> 2), c));
+            if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
+          }
+          __syncwarp();  // transpose box and operand box free again
+          if (oe >= 0 && lane == 0) issue_other();
+          const bool full_blk = vec_ok && rows_in && q0 + CW <= QQ;
+          const int gq = q0 + c * 4;
+          auto put = [&](int e) {
+            float* d0 = dp[e] + q0;
+            if (full_blk) {
+              if (ostream) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) __stcs(reinterpret_cast<float4*>(d0 + i * st8[e]), x[i]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) *reinterpret_cast<float4*>(d0 + i * st8[e]) = x[i];
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                if (prow0 + i * 8 + (lane >> 2) >= PP) continue;
+                float* d = d0 + i * st8[e];
+                if (vec_ok && gq + 4 <= QQ) {
+                  *reinterpret_cast<float4*>(d) = x[i];
+                } else {
+                  if (gq < QQ) d[0] = x[i].x;
+                  if (gq + 1 < QQ) d[1] = x[i].y;
+                  if (gq + 2 < QQ) d[2] = x[i].z;
+                  if (gq + 3 < QQ) d[3] = x[i].w;
+                }
+              }
+            }
+          };
+          switch (chain) {
+            case 0:
+              put(0);
+              break;
+            case 1:
+              put(0);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) { x[i].x = tanhf(x[i].x); x[i].y = tanhf(x[i].y); x[i].z = tanhf(x[i].z); x[i].w = tanhf(x[i].w); }
+              put(1);
+              break;
+            case 2:
+              put(0);
+              epi_apply4(EPI_DTANH, x, ox, 0.f);
+              put(1);
+              break;
+            case 3:  // gw -> wd = lr * gw -> w_next = w - wd
+              put(0);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) { x[i].x *= s0; x[i].y *= s0; x[i].z *= s0; x[i].w *= s0; }
+              put(1);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) { x[i].x = ox[i].x - x[i].x; x[i].y = ox[i].y - x[i].y; x[i].z = ox[i].z - x[i].z; x[i].w = ox[i].w - x[i].w; }
+              put(2);
+              break;
+            case 4:
+              put(0);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) { x[i].x = tanhf(x[i].x); x[i].y = tanhf(x[i].y); x[i].z = tanhf(x[i].z); x[i].w = tanhf(x[i].w); }
+              put(1);
+              epi_apply4(EPI_DTANH, x, ox, 0.f);
+              put(2);
+              break;
+            default:
+              put(0);
+#pragma unroll
+              for (int e = 1; e <= kMaxEpi; ++e) {
+                if (e >= nout) break;
+                epi_apply4(eop[e - 1], x, ox, esc[e - 1]);
+                put(e);
+              }
+          }
+        }
+        continue;
+      }
+#pragma unroll 1
+      for (int c0 = c_begin; c0 < c_end; c0 += CSTEP) {
         const int q0 = sg.tq * BN + c0;
         float o[CW];
         if (oe >= 0 && q0 < QQ) {
           if (o_tma) {
-            // the box was requested one chunk ahead; read my row, then request the next box
-            mbar_wait(&other_bar[ew], o_used & 1);
-            const uint32_t ob = smem_u32(other_stage + ew * kOutStage);
+            // the box was requested ODEPTH chunks ahead; read my row, refill the slot
+            mbar_wait(&other_bar[ew * ODEPTH + o_slot], o_phase);
+            const uint32_t ob = smem_u32(other_stage + (ew * ODEPTH + o_slot) * kOutStage);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
               const float4 x = lds128(ob + box_off(lane, j));
               o[4 * j] = x.x; o[4 * j + 1] = x.y; o[4 * j + 2] = x.z; o[4 * j + 3] = x.w;
             }
-            ++o_used;
+            if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
             __syncwarp();
-            if (lane == 0) {
-              if (c0 + CW < c_end && q0 + CW < QQ) {
-                fence_proxy_async_smem();  // same segment: the next box of this tile
-                mbar_arrive_expect_tx(&other_bar[ew], kOutStage);
-                tma_load_2d_hint(other_stage + ew * kOutStage, omap, &other_bar[ew], q0 + CW, prow0, o_policy);
-              } else {
-                issue_other(si + 1, c_begin);
-              }
-            }
+            if (lane == 0) issue_other();
           } else {
             load_chunk(pr.epi[oe].other, pr.epi[oe].o_rs, pr.epi[oe].o_cs, p, q0, PP, QQ, o);
           }
@@ -498,17 +736,17 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
 #pragma unroll
           for (int j = 0; j < CW; ++j) v[j] = 0.f;
         }
-        if (c0 + CW >= c_end) {
+        if (c0 + CSTEP >= c_end) {
           // accumulator drained: hand it back to the MMA warp before the global traffic
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+          if (lane == 0) mbar_arrive_cluster(tmem_empty_lead + acc * 8);
         }
         if (sg.kind == SEG_HEAD) {
           for (int pp = 0; pp < sg.n_parts; ++pp) {
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
-              const float4 x = __ldcg(ws_ptr(ws, sg.slot + pp, BN, c0, j, row));
+              const float4 x = __ldcg(ws_ptr(ws, wslot(sg.slot + pp), BN, c0, j, row));
               v[4 * j] += x.x; v[4 * j + 1] += x.y; v[4 * j + 2] += x.z; v[4 * j + 3] += x.w;
             }
           }
@@ -531,32 +769,50 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // both CTAs done with the pair's TMEM and barriers
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    else tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
 using KernelFn = void (*)(const GemmProblem*, const GemmSeg*, const int*, float*, unsigned*, int, int, int);
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool PAIR>
 KernelFn pick(bool p_mn, bool q_mn) {
-  if (!p_mn && !q_mn) return gemm_tf32_kernel<BN, false, false, SPLIT>;
-  if (!p_mn && q_mn) return gemm_tf32_kernel<BN, false, true, SPLIT>;
-  if (p_mn && !q_mn) return gemm_tf32_kernel<BN, true, false, SPLIT>;
-  return gemm_tf32_kernel<BN, true, true, SPLIT>;
+  if (!p_mn && !q_mn) return gemm_tf32_kernel<BN, false, false, SPLIT, PAIR>;
+  if (!p_mn && q_mn) return gemm_tf32_kernel<BN, false, true, SPLIT, PAIR>;
+  if (p_mn && !q_mn) return gemm_tf32_kernel<BN, true, false, SPLIT, PAIR>;
+  return gemm_tf32_kernel<BN, true, true, SPLIT, PAIR>;
 }
 
-KernelFn kernel_for(int bn, bool p_mn, bool q_mn, bool split) {
+KernelFn kernel_for(int bn, bool p_mn, bool q_mn, bool split, bool pair) {
+  if (pair) {
+    if (bn != 256 || split) throw std::runtime_error("gemm: CTA-pair tiles are 256 x 256 TF32 only");
+    return pick<256, false, true>(p_mn, q_mn);
+  }
   switch (bn) {
-    case 32: return split ? pick<32, true>(p_mn, q_mn) : pick<32, false>(p_mn, q_mn);
-    case 64: return split ? pick<64, true>(p_mn, q_mn) : pick<64, false>(p_mn, q_mn);
-    case 128: return split ? pick<128, true>(p_mn, q_mn) : pick<128, false>(p_mn, q_mn);
-    case 256: return split ? pick<256, true>(p_mn, q_mn) : pick<256, false>(p_mn, q_mn);
+    case 32: return split ? pick<32, true, false>(p_mn, q_mn) : pick<32, false, false>(p_mn, q_mn);
+    case 64: return split ? pick<64, true, false>(p_mn, q_mn) : pick<64, false, false>(p_mn, q_mn);
+    case 128: return split ? pick<128, true, false>(p_mn, q_mn) : pick<128, false, false>(p_mn, q_mn);
+    case 256: return split ? pick<256, true, false>(p_mn, q_mn) : pick<256, false, false>(p_mn, q_mn);
   }
   throw std::runtime_error("gemm: unsupported tile width " + std::to_string(bn));
 }
+
+unsigned g_dbg_lbo = 0, g_dbg_sbo = 0;
+bool g_no_tma_store = false;
+int g_prefetch = -1;  // -1: default (off)
+int g_stages = 0;     // 0: as many as fit
+int g_sleep = 1;      // epilogue waits with nanosleep back-off
+bool g_no_3d = false;
+int g_other_promo = 0;     // L2 promotion of the epilogue operand map (0 none .. 3 256 B)
+bool g_no_stream = false;  // disable evict-first stores / operand policies
+const CUtensorMapL2promotion kOtherPromo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+bool g_no_pair = false;
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -588,7 +844,9 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            sw64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                 : mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           // 64-byte operand rows: no promotion (a promoted 256 B line would be
+                           // evicted, evict-first, before the next chunks use it)
+                           sw64 ? kOtherPromo[g_other_promo & 3] : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
@@ -616,13 +874,6 @@ struct Role {
   bool mn;  // contiguous dim is the row (M/N) dim rather than K
 };
 
-unsigned g_dbg_lbo = 0, g_dbg_sbo = 0;
-bool g_no_tma_store = false;
-int g_prefetch = -1;  // -1: default (off)
-int g_stages = 0;     // 0: as many as fit
-int g_sleep = 1;      // epilogue waits with nanosleep back-off
-bool g_no_3d = false;
-
 inline bool epi_needs_other_host(int op) { return op >= EPI_ADD; }
 
 struct SchedCol { int prob, tq, tp0, ntp, kb; };
@@ -638,8 +889,11 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 2) g_prefetch = int(sbo) - 1;
   if (lbo == 4) g_stages = int(sbo);
   if (lbo == 5) g_sleep = (sbo != 2);  // (5,2) spin without back-off
+  if (lbo == 6) g_no_pair = (sbo == 1);  // (6,1) single-CTA tiles only
+  if (lbo == 7) g_other_promo = sbo > 0 ? int(sbo) - 1 : 0;  // (7,n) operand promotion n-1
+  if (lbo == 8) g_no_stream = (sbo == 1);  // (8,1) no L2 streaming hints
   if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
-  if (lbo >= 1 && lbo <= 5) g_dbg_lbo = g_dbg_sbo = 0;
+  if (lbo >= 1 && lbo <= 8) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
 bool gemm_view_ok(const MatView& v) {
@@ -768,6 +1022,11 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   const long long Q0 = g.swap ? M0 : N0;
   g.bn = Q0 <= 32 ? 32 : Q0 <= 64 ? 64 : Q0 <= 128 ? 128 : 256;
   g.nprob = int(specs.size());
+  // CTA pairs (256 x 256 tiles, half the operand bytes per SM) for wide TF32 problems
+  const long long P0 = g.swap ? N0 : M0;
+  g.pair = !split && !g_no_pair && g.bn == 256 && P0 >= 256 && num_sms >= 4;
+  const int pbm = g.pair ? 2 * BM : BM;
+  const int bnh = g.pair ? g.bn / 2 : g.bn;  // B columns one CTA stages (its TMA box)
 
   std::vector<CUtensorMap> maps(2 * specs.size());
   std::vector<CUtensorMap> store_maps;  // epilogue operand maps
@@ -801,15 +1060,15 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
       make_map(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, 32, rp.mn ? 32 : BM, rp.mn);
     }
     if (rq.mn && rq.inner % 32 == 0 && !g_no_3d) {
-      make_map_mn3d(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, g.bn / 32);
+      make_map_mn3d(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, bnh / 32);
       pr.b3d = 1;
     } else {
-      make_map(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, 32, rq.mn ? 32 : g.bn, rq.mn);
+      make_map(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, 32, rq.mn ? 32 : bnh, rq.mn);
     }
     pr.P = int(g.swap ? N : M);
     pr.Q = int(g.swap ? M : N);
     pr.K = int(K);
-    pr.tiles_p = int((pr.P + BM - 1) / BM);
+    pr.tiles_p = int((pr.P + pbm - 1) / pbm);
     pr.tiles_q = int((pr.Q + g.bn - 1) / g.bn);
     pr.kb_total = int((K + BK - 1) / BK);
     pr.out = s.c;
@@ -861,18 +1120,19 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     }
     const double kStream = 48.0 * (1 << 20), kOutStream = 64.0 * (1 << 20);
     for (auto& pr : probs) {
-      pr.a_stream = pb > kStream;
-      pr.b_stream = qb > kStream;
-      pr.out_stream = ob > kOutStream;
+      pr.a_stream = pb > kStream && !g_no_stream;
+      pr.b_stream = qb > kStream && !g_no_stream;
+      pr.out_stream = ob > kOutStream && !g_no_stream;
     }
   }
-  g.sched = gemm_schedule(probs, g.bn, num_sms, 0);
-  g.units = g.sched.grid;
-  g.ws_floats = size_t(g.sched.nslots) * BM * g.bn;
+  g.sched = gemm_schedule(probs, g.bn, g.pair ? num_sms / 2 : num_sms, 0);
+  g.units = g.sched.grid * (g.pair ? 2 : 1);
+  const size_t halves = size_t(g.sched.nslots) * (g.pair ? 2 : 1);  // one BM x BN slot per CTA
+  g.ws_floats = halves * BM * g.bn;
   if (g.sched.nslots) {
     CUDA_CHECK(cudaMalloc(&g.d_ws, g.ws_floats * sizeof(float)));
-    CUDA_CHECK(cudaMalloc(&g.d_flags, size_t(g.sched.nslots) * sizeof(unsigned)));
-    CUDA_CHECK(cudaMemset(g.d_flags, 0, size_t(g.sched.nslots) * sizeof(unsigned)));
+    CUDA_CHECK(cudaMalloc(&g.d_flags, halves * sizeof(unsigned)));
+    CUDA_CHECK(cudaMemset(g.d_flags, 0, halves * sizeof(unsigned)));
   }
   const size_t nload = maps.size();
   maps.insert(maps.end(), store_maps.begin(), store_maps.end());
@@ -893,22 +1153,50 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   CUDA_CHECK(cudaMemcpy(g.d_segs, g.sched.segs.data(), g.sched.segs.size() * sizeof(GemmSeg), cudaMemcpyHostToDevice));
   CUDA_CHECK(cudaMalloc(&g.d_seg_off, g.sched.seg_off.size() * sizeof(int)));
   CUDA_CHECK(cudaMemcpy(g.d_seg_off, g.sched.seg_off.data(), g.sched.seg_off.size() * sizeof(int), cudaMemcpyHostToDevice));
-  g.stages = stages_for(g.bn, split, g.other_smem);
+  const int bn_stage = g.pair ? g.bn / 2 : g.bn;  // B columns staged per CTA
+  // operand ring as deep as possible while the mainloop keeps >= 3 stages (>= 1 box)
+  g.odepth = 0;
+  if (g.other_smem) {
+    g.odepth = 1;
+    for (int d = kOtherDepth; d > 1; --d)
+      if (stages_for(bn_stage, split, d) >= 3) { g.odepth = d; break; }
+  }
+  g.stages = stages_for(bn_stage, split, g.odepth);
   if (g_stages > 0) g.stages = std::min(g.stages, g_stages);
-  g.smem_bytes = smem_for(g.bn, split, g.other_smem, g.stages);
+  if (g.stages < 1) throw std::runtime_error("gemm: tile does not fit in shared memory");
+  g.smem_bytes = smem_for(bn_stage, split, g.odepth, g.stages);
   g.prefetch = g_prefetch >= 0 ? g_prefetch : 0;
   g.threads = threads_for(split);
-  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, split);
+  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, split, g.pair);
   // the attribute is per function and launches of one instantiation differ in smem: allow the max
   CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)));
   return g;
 }
 
 void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
-  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split);
-  fn<<<g.sched.grid, g.threads, g.smem_bytes, stream>>>(
-      static_cast<const GemmProblem*>(g.d_problems), static_cast<const GemmSeg*>(g.d_segs),
-      g.d_seg_off, g.d_ws, g.d_flags, g.stages, g.prefetch, (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0));
+  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair);
+  const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
+  const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
+  const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4);
+  if (g.pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(2 * g.sched.grid));
+    cfg.blockDim = dim3(unsigned(g.threads));
+    cfg.dynamicSmemBytes = g.smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, probs, segs, static_cast<const int*>(g.d_seg_off), g.d_ws,
+                                  g.d_flags, g.stages, g.prefetch, flags));
+  } else {
+    fn<<<g.sched.grid, g.threads, g.smem_bytes, stream>>>(probs, segs, g.d_seg_off, g.d_ws, g.d_flags,
+                                                          g.stages, g.prefetch, flags);
+  }
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -94,12 +94,14 @@ struct GemmLaunch {
   int bn = 0;
   bool split = false;           // 3xTF32
   bool p_mn = false, q_mn = false, swap = false;
+  bool pair = false;            // CTA-pair (cta_group::2) 256 x 256 tiles
   int units = 0;                // CTAs launched
   int nprob = 0;
   int threads = 256;
   int stages = 0;               // smem ring depth
   int prefetch = 0;             // k-blocks of L2 prefetch ahead of the ring (0 = off)
   bool other_smem = false;      // epilogue operand staged through TMA
+  int odepth = 0;               // its boxes in flight per epilogue warp
   GemmSchedule sched;
   void* d_problems = nullptr;   // GemmProblem[nprob] on device
   void* d_tmaps = nullptr;      // 2*nprob CUtensorMap on device

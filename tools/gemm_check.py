@@ -90,6 +90,9 @@ def diag():
 def main():
     if "--diag" in sys.argv:
         diag()
+    for kv in filter(None, os.environ.get("TPX_GEMM_KNOBS", "").split(",")):
+        k, v = kv.split(":")  # debug knobs of gemm.cu (tpx_debug_gemm_mn_desc)
+        native.lib().tpx_debug_gemm_mn_desc(ctypes.c_uint(int(k)), ctypes.c_uint(int(v)))
     if "--one" in sys.argv:
         # --one M N K ta tb [epi,...]: one timed configuration (for ncu)
         i = sys.argv.index("--one")
@@ -147,8 +150,7 @@ def main():
         shapes = [((512, 8192, 8192, False, False), None), ((512, 8192, 8192, False, True), None),
                   ((8192, 8192, 512, True, False), [3, 6]), ((64, 8192, 8192, False, False), None),
                   ((4096, 4096, 4096, False, False), None), ((8192, 8192, 8192, False, True), None)]
-        variants = [("base", []), ("st3", [(4, 3)]), ("spin", [(5, 2)]), ("no3d", [(3, 1)]),
-                    ("direct", [(1, 1)])]
+        variants = [("base", []), ("nopair", [(6, 1)]), ("spin", [(5, 2)]), ("st4", [(4, 4)])]
         res = {}
         for rep in range(2):
             for name, knobs in variants:
