@@ -159,6 +159,61 @@ def run_reference(args):
     }), flush=True)
 
 
+def kernel_rooflines(r, tensor_peak, hbm_peak):
+    """Per GEMM class (fwd / bwd_x / bwd_w: the op id without its layer number) of this rank's
+    lowered step: launches per step, mean device ms per launch (CUDA events around every lowered
+    step, on the executor's stream), algorithmic FLOPs and bytes per launch (operands read once,
+    every fused output written once, describe()), the bound (the larger of FLOPs / tensor peak
+    and bytes / HBM peak) and the achieved rate in that unit.  Returns (list, dominant class)."""
+    import re
+    total = sum(r["step_ms"]) or 1.0
+    cls = {}
+    for st, ms in zip(r["steps_desc"], r["step_ms"]):
+        if st["kind"] != "gemm":
+            continue
+        name = re.sub(r"\d+$", "", st["op"])
+        c = cls.setdefault(name, {"class": name, "launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0,
+                                  "what": f"{'T' if st['ta'] else 'N'}{'T' if st['tb'] else 'N'} "
+                                          f"{'x'.join(str(v) for v in st['shapes'][0][:3])}, "
+                                          f"{st['shapes'][0][3]} fused epilogue stages, "
+                                          f"{'CTA pair' if st.get('pair') else '1 CTA'}"})
+        c["launches"] += 1
+        c["ms"] += ms
+        c["flops"] += st.get("flops", 0.0)
+        c["bytes"] += st.get("min_bytes", 0.0)
+    out = []
+    for c in cls.values():
+        n = c["launches"]
+        t_tc = c["flops"] / (tensor_peak * 1e12)
+        t_hbm = c["bytes"] / (hbm_peak * 1e9)
+        bound = "tensor" if t_tc >= t_hbm else "hbm"
+        sec = c["ms"] / 1e3
+        ach = c["flops"] / sec / 1e12 if bound == "tensor" else c["bytes"] / sec / 1e9
+        pk = tensor_peak if bound == "tensor" else hbm_peak
+        out.append({"class": c["class"], "what": c["what"], "launches_per_step": n, "ms": c["ms"] / n,
+                    "share": c["ms"] / total, "bound": bound, "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+                    "achieved": ach, "peak": pk, "frac": ach / pk,
+                    "per_launch": {"flops": c["flops"] / n, "bytes": c["bytes"] / n},
+                    "tflops": c["flops"] / sec / 1e12, "gbs": c["bytes"] / sec / 1e9,
+                    "roofline_ms": max(t_tc, t_hbm) * 1e3 / n})
+    out.sort(key=lambda c: -c["share"])
+    return out, (out[0] if out else None)
+
+
+def step_roofline_ms(kernels):
+    return sum(k["roofline_ms"] * k["launches_per_step"] for k in kernels)
+
+
+def measured_traffic():
+    """DRAM bytes per launch of each GEMM class from the committed ncu --set full capture
+    (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
 def timed(fn, stream, steps, barrier):
     import torch
     barrier()
@@ -238,15 +293,18 @@ def main():
              "stats": st, "clocks": clk.summary()}
         # per-launch timing pass (events between every lowered step) for the roofline
         ex.enable_timing(True)
-        g_ms, t_ms = [], []
+        g_ms, t_ms, per_step = [], [], []
         for _ in range(5):
             ex.execute()
             t = ex.last_timing()
             g_ms.append(t["gemm_ms"])
             t_ms.append(t["total_ms"])
+            per_step.append(ex.last_step_times())
         ex.enable_timing(False)
         r["gemm_ms"] = statistics.median(g_ms)
         r["timed_total_ms"] = statistics.median(t_ms)
+        r["step_ms"] = [statistics.median(x) for x in zip(*per_step)]
+        r["steps_desc"] = ex.describe()["main"]["steps"]
         # e2e through the public API: host (pinned) x0 in, network output out, every step
         plan = json.loads(text)
         mine = set(ex.my_devices())
@@ -297,9 +355,10 @@ def main():
         return
     o, d = res["opt"], res["data"]
     flops = o["stats"]["gemm_flops"]
-    achieved = flops / (o["gemm_ms"] / 1e3) / 1e12
     tf32_peak = bf16_peak / 2
     peak = tf32_peak if prec == 0 else tf32_peak / 3
+    kernels, dom = kernel_rooflines(o, peak, hbm_peak)
+    traffic = (measured_traffic().get(dom["class"]) or {}).get("dram_bytes_per_launch") if dom else None
     line = {
         "metric": METRIC, "value": o["value"], "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": o["ms_per_step"],
@@ -314,15 +373,19 @@ def main():
         "fetch_bytes_total": o["stats"]["fetch_bytes_total"],
         "e2e": o["e2e"],
         "gpu_launches": int(o["stats"]["n_kernel_launches"] * args.steps),
-        "roofline": {"bound": "tensor", "kernel": "tcgen05 tile GEMM (gemm_tf32_kernel)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": None,
-                     "peak_basis": (f"{peak_kind} bf16 {bf16_peak} TFLOP/s / 2 (kind::tf32 issues at half the "
-                                    f"kind::f16 rate)" + (" / 3 (3xTF32 split)" if prec else "")),
+        "roofline": {"bound": dom["bound"], "kernel": f"tcgen05 tile GEMM, {dom['class']} ({dom['what']})",
+                     "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
+                     "frac": dom["achieved"] / dom["peak"], "traffic": traffic,
+                     "algorithmic_per_launch": dom["per_launch"], "avg_launch_ms": dom["ms"],
+                     "share_of_step": dom["share"],
+                     "peak_basis": (f"{peak_kind} MEASURED_PEAKS: HBM {hbm_peak} GB/s; tensor = bf16 {bf16_peak} "
+                                    f"TFLOP/s / 2 (kind::tf32 issues at half the kind::f16 rate)"
+                                    + (" / 3 (3xTF32 split)" if prec else "")),
+                     "kernels": kernels,
                      "flops_per_step": flops, "gemm_ms_per_step": o["gemm_ms"],
                      "gemm_share_of_step": o["gemm_ms"] / o["timed_total_ms"],
-                     "step_roofline_ms": flops / (peak * 1e12) * 1e3,
-                     "step_frac": (flops / (peak * 1e12) * 1e3) / o["ms_per_step"]},
+                     "step_roofline_ms": step_roofline_ms(kernels),
+                     "step_frac": step_roofline_ms(kernels) / o["ms_per_step"]},
         "clocks": o["clocks"],
         "cpu_baseline": cpu,
     }

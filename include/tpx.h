@@ -117,6 +117,9 @@ int tpx_synchronize(tpx_plan* plan);
 /* Per-step device timing of the last tpx_execute (events around each step): total ms and
  * ms spent in GEMM launches. */
 int tpx_last_timing(const tpx_plan* plan, double* total_ms, double* gemm_ms, double* copy_ms);
+/* Per-step device times (ms) of the last timed execution, in the order of
+ * tpx_plan_describe()'s "main" steps; fills min(n, *n_steps) entries. */
+int tpx_last_step_times(const tpx_plan* plan, double* ms, int64_t n, int64_t* n_steps);
 int tpx_enable_timing(tpx_plan* plan, int on);
 
 /* ---------------------------------------------------------------- kernel-level entry points

@@ -208,6 +208,14 @@ TPX_API int tpx_enable_timing(tpx_plan* plan, int on) {
   return tpx::guard([&] { rt(plan).timing = on != 0; });
 }
 
+TPX_API int tpx_last_step_times(const tpx_plan* plan, double* ms, int64_t n, int64_t* n_steps) {
+  return tpx::guard([&] {
+    const tpx::PlanRt& P = rt(plan);
+    *n_steps = int64_t(P.last_step_ms.size());
+    for (int64_t i = 0; i < n && i < *n_steps; ++i) ms[i] = P.last_step_ms[size_t(i)];
+  });
+}
+
 TPX_API int tpx_last_timing(const tpx_plan* plan, double* total_ms, double* gemm_ms, double* copy_ms) {
   return tpx::guard([&] {
     const tpx::PlanRt& P = rt(plan);

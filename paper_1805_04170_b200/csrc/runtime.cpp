@@ -746,9 +746,11 @@ void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
   }
   CUDA_CHECK(cudaEventSynchronize(P.events[n]));
   P.last_total_ms = P.last_gemm_ms = P.last_copy_ms = 0;
+  P.last_step_ms.assign(n, 0.0);
   for (size_t i = 0; i < n; ++i) {
     float ms = 0;
     CUDA_CHECK(cudaEventElapsedTime(&ms, P.events[i], P.events[i + 1]));
+    P.last_step_ms[i] = ms;
     P.last_total_ms += ms;
     if (prog.steps[i].kind == ST_GEMM) P.last_gemm_ms += ms;
     else if (prog.steps[i].kind == ST_NARY || prog.steps[i].kind == ST_XCHG) P.last_copy_ms += ms;
@@ -860,7 +862,8 @@ std::string describe(const PlanRt& P) {
         s << "],\"ta\":" << (specs.empty() ? 0 : specs[0].ta) << ",\"tb\":" << (specs.empty() ? 0 : specs[0].tb);
         if (size_t(st.idx) < prog.gemm.size()) {
           const GemmLaunch& gl = prog.gemm[size_t(st.idx)];
-          s << ",\"bn\":" << gl.bn << ",\"swap\":" << gl.swap << ",\"units\":" << gl.units
+          s << ",\"bn\":" << gl.bn << ",\"swap\":" << gl.swap << ",\"pair\":" << gl.pair
+            << ",\"flops\":" << gl.flops << ",\"min_bytes\":" << gl.min_bytes << ",\"units\":" << gl.units
             << ",\"stream_k\":" << gl.sched.stream_k << ",\"group\":" << gl.sched.group
             << ",\"segments\":" << gl.sched.segs.size() << ",\"partial_slots\":" << gl.sched.nslots;
         }

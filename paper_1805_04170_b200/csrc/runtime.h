@@ -92,6 +92,7 @@ struct PlanRt {
   bool timing = false;
   std::vector<cudaEvent_t> events;
   double last_total_ms = 0, last_gemm_ms = 0, last_copy_ms = 0;
+  std::vector<double> last_step_ms;  // per lowered step of the last timed run
   float* io_tmp = nullptr;
   size_t io_tmp_elems = 0;
   cudaStream_t stream = nullptr;

@@ -127,6 +127,14 @@ class PlanExecutor:
     def enable_timing(self, on: bool = True):
         check(lib().tpx_enable_timing(self._h, int(on)))
 
+    def last_step_times(self):
+        """Per lowered step device ms of the last timed execute() (describe()['main']['steps'] order)."""
+        n = ctypes.c_int64()
+        check(lib().tpx_last_step_times(self._h, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_double * max(n.value, 1))()
+        check(lib().tpx_last_step_times(self._h, buf, n.value, ctypes.byref(n)))
+        return list(buf[: n.value])
+
     def last_timing(self):
         t, g, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         check(lib().tpx_last_timing(self._h, ctypes.byref(t), ctypes.byref(g), ctypes.byref(c)))
