@@ -79,6 +79,8 @@ typedef struct tpx_plan tpx_plan;
  * GPU). */
 #define TPX_FLAG_FUSE 1
 #define TPX_FLAG_FORCE_XCHG 2
+/* Convolutions on CUDA cores (direct loops) instead of im2col + tcgen05 GEMM (cross-check). */
+#define TPX_FLAG_DIRECT_CONV 4
 int tpx_load_plan(tpx_ctx* ctx, const char* plan_json, size_t len, int precision, int flags,
                   tpx_plan** out);
 int tpx_plan_free(tpx_plan* plan);

@@ -837,7 +837,9 @@ EncodeTiledFn encode_fn() {
 void make_map(CUtensorMap* m, const float* base, long long inner, long long outer,
               long long row_stride, int box_inner, int box_outer, bool mn_major, bool sw64 = false) {
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(std::max<long long>(row_stride, inner) * 4)};
+  // a single row's stride is never used, but the encoder wants it 16-byte aligned
+  const long long rs = outer > 1 ? std::max<long long>(row_stride, inner) : (inner + 3) / 4 * 4;
+  cuuint64_t strides[1] = {(cuuint64_t)(rs * 4)};
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
@@ -857,7 +859,8 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
 void make_map_mn3d(CUtensorMap* m, const float* base, long long inner, long long outer,
                    long long row_stride, int nchunk) {
   cuuint64_t dims[3] = {32, (cuuint64_t)outer, (cuuint64_t)(inner / 32)};
-  cuuint64_t strides[2] = {(cuuint64_t)(std::max<long long>(row_stride, inner) * 4), 128};
+  const long long rs = outer > 1 ? std::max<long long>(row_stride, inner) : inner;
+  cuuint64_t strides[2] = {(cuuint64_t)(rs * 4), 128};
   cuuint32_t box[3] = {32, 32, (cuuint32_t)nchunk};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,

@@ -188,6 +188,53 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restri
   const ConvDesc& d = ds[di];
   const int64_t e = (int64_t(blockIdx.x) - d.tile_begin) * kThreads + threadIdx.x;
   if (e >= d.n) return;
+  if (d.mode >= CONV_IM2COL_ROWS) {
+    // data movement of the tensor-core conv lowering; consecutive threads write consecutive
+    // output elements (coalesced stores), the gathers hit L1/L2 (each input element is read
+    // U*V times by neighbouring threads)
+    if (d.mode == CONV_COL2IM) {
+      const int64_t C = d.p[0], U = d.p[1], V = d.p[2], Yo = d.p[3], Xo = d.p[4], pitch = d.p[5];
+      const int64_t H = Yo + U - 1, W = Xo + V - 1;
+      const int64_t x = e % W;
+      int64_t t = e / W;
+      const int64_t y = t % H;
+      t /= H;
+      const int64_t c = t % C;
+      const int64_t nb = t / C;
+      const float* col = d.a.ptr + nb * (Yo * Xo * pitch);
+      float acc = 0.f;
+      for (int64_t u = 0; u < U; ++u) {
+        const int64_t yy = y - u;
+        if (yy < 0 || yy >= Yo) continue;
+        for (int64_t v = 0; v < V; ++v) {
+          const int64_t xx = x - v;
+          if (xx < 0 || xx >= Xo) continue;
+          acc += __ldg(col + (yy * Xo + xx) * pitch + (c * U + u) * V + v);
+        }
+      }
+      d.out[e] = acc;
+      return;
+    }
+    const int64_t U = d.p[0], V = d.p[1], Yo = d.p[2], Xo = d.p[3], pitch = d.p[4];
+    const int64_t C = d.a.shape[1], NB = d.a.shape[0], K = C * U * V, YX = Yo * Xo;
+    int64_t nb, yx, k, dst;
+    if (d.mode == CONV_IM2COL_ROWS) {
+      k = e % K;
+      const int64_t r = e / K;
+      yx = r % YX;
+      nb = r / YX;
+      dst = r * pitch + k;
+    } else {
+      const int64_t m = e % (NB * YX);
+      k = e / (NB * YX);
+      yx = m % YX;
+      nb = m / YX;
+      dst = k * pitch + m;
+    }
+    const int64_t v = k % V, u = (k / V) % U, c = k / (U * V);
+    d.out[dst] = at4(d.a, nb, c, yx / Xo + u, yx % Xo + v);
+    return;
+  }
   const int64_t o3 = e % d.oshape[3];
   int64_t t = e / d.oshape[3];
   const int64_t o2 = t % d.oshape[2];

@@ -89,13 +89,23 @@ void init_run(const InitBatch& b, cudaStream_t s);
 void init_free(InitBatch& b);
 uint64_t fnv1a(const char* s, size_t n);
 
-enum ConvModeCode : int { CONV_FWD = 0, CONV_GRAD_W = 1, CONV_GRAD_IN = 2 };
+// Direct convolution modes (run_conv on CUDA cores, kept as the cross-check path) and the
+// data-movement kernels of the tensor-core lowering (conv = im2col + tcgen05 GEMM [+ col2im]).
+enum ConvModeCode : int {
+  CONV_FWD = 0, CONV_GRAD_W = 1, CONV_GRAD_IN = 2,
+  CONV_IM2COL_ROWS = 3,  // out[(n*Yo*Xo + y*Xo+x)*pitch + c*U*V+u*V+v] = a[n,c,y+u,x+v]
+  CONV_IM2COL_COLS = 4,  // out[(c*U*V+u*V+v)*pitch + n*Yo*Xo + y*Xo+x] = a[n,c,y+u,x+v]
+                         //   (p = U,V,Yo,Xo,pitch; pitch >= the row length, 16-byte rows)
+  CONV_COL2IM = 5,       // out[n,c,y,x] = sum_{u,v} col[(n*Yo*Xo + (y-u)*Xo+(x-v))*pitch + c*U*V+u*V+v]
+                         //   (a.ptr = col, p = C,U,V,Yo,Xo,pitch; taps in ascending (u, v) order)
+};
 struct ConvDesc {
   int mode;
   StridedView a, b;   // rank-4 operands as run_conv receives them
-  float* out;         // contiguous rank-4 output
+  float* out;         // contiguous output
   int64_t oshape[4];
   int64_t n;          // output elements
+  int64_t p[6];       // mode parameters (see ConvModeCode)
   int64_t tile_begin;
 };
 struct ConvBatch {

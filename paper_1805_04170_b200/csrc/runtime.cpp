@@ -56,7 +56,7 @@ MatView mat_view(const StridedView& v) {
 
 // Classes of an open segment, flushed in this order (each may read values produced by an
 // earlier class of the same segment, never by its own or a later class).
-enum Cls { C_PRE = 0, C_COMPUTE = 1, C_PACK = 2, C_XCHG = 3, C_COPY = 4, C_REDUCE = 5, C_N = 6 };
+enum Cls { C_PRE = 0, C_COMPUTE = 1, C_POST = 2, C_PACK = 3, C_XCHG = 4, C_COPY = 5, C_REDUCE = 6, C_N = 7 };
 
 struct Lowerer {
   PlanRt& P;
@@ -75,6 +75,7 @@ struct Lowerer {
 
   // open segment
   NaryBatch o_pre, o_ew, o_pack, o_copy, o_reduce;
+  ConvBatch o_prec, o_post;    // im2col before / col2im after a conv's GEMM
   XchgGroup o_xchg;
   int o_gemm = -1;             // open gemm batch index
   ConvBatch o_conv;
@@ -85,7 +86,8 @@ struct Lowerer {
 
   Lowerer(PlanRt& p, Program& pr, bool d)
       : P(p), pl(p.plan), C(*p.ctx), prog(pr), dry(d),
-        fuse(p.flags & 1), force_xchg(p.flags & 2) {}
+        fuse(p.flags & 1), force_xchg(p.flags & 2), tc_conv(!(p.flags & 4)) {}
+  bool tc_conv;
 
   float* alloc_bytes(size_t bytes) {
     const size_t off = (P.arena_used + kAlign - 1) / kAlign * kAlign;
@@ -121,6 +123,14 @@ struct Lowerer {
       for (int n : o_nodes[c]) P.avail_step[size_t(n)] = s;
     };
     emit_nary(o_pre, o_pre_op, "materialize", C_PRE);
+    auto emit_conv = [&](ConvBatch& b, const std::string& op, const std::string& what, Cls c) {
+      if (b.descs.empty()) return;
+      prog.conv.push_back(std::move(b));
+      b = ConvBatch{};
+      const int s = add_step(ST_CONV, int(prog.conv.size()) - 1, op, what);
+      for (int n : o_nodes[c]) P.avail_step[size_t(n)] = s;
+    };
+    emit_conv(o_prec, o_pre_op, "im2col", C_PRE);
     if (o_kind == 0) {
       const int s = add_step(ST_GEMM, o_gemm, o_op, "gemm");
       gemm_step[size_t(o_gemm)] = s;
@@ -133,6 +143,7 @@ struct Lowerer {
       const int s = add_step(ST_CONV, int(prog.conv.size()) - 1, o_op, "conv");
       for (int n : o_nodes[C_COMPUTE]) P.avail_step[size_t(n)] = s;
     }
+    emit_conv(o_post, o_op, "col2im", C_POST);
     emit_nary(o_pack, seg_op, "pack", C_PACK);
     if (!o_xchg.x.empty()) {
       prog.xchg.push_back(std::move(o_xchg));
@@ -187,6 +198,10 @@ struct Lowerer {
 
     if (op.kind == OpKind::elementwise && fuse && try_fuse(ni, op)) return;
 
+    if (op.kind == OpKind::conv && tc_conv) {
+      lower_conv_gemm(ni, op);
+      return;
+    }
     const int kind = op.kind == OpKind::matmul ? 0 : op.kind == OpKind::elementwise ? 1 : 2;
     if (o_kind >= 0 && (o_kind != kind || o_op != op.id)) flush();
     if (o_kind < 0) {
@@ -251,6 +266,164 @@ struct Lowerer {
       o_conv.flops += 2.0 * contr;
     }
     produced(ni, C_COMPUTE);
+  }
+
+  // 2-D view of a rank-4 filter K[o, c, u, v] as [o, c*u*v] when (c, u, v) is contiguous and
+  // the rows are TMA-addressable.
+  static bool filter_mat(const StridedView& k, MatView& m) {
+    if (k.rank != 4 || k.st[3] != 1 || k.st[2] != k.shape[3] || k.st[1] != k.shape[2] * k.shape[3]) return false;
+    m.ptr = k.ptr;
+    m.rows = k.shape[0];
+    m.cols = k.shape[1] * k.shape[2] * k.shape[3];
+    m.rs = k.st[0];
+    m.cs = 1;
+    return gemm_view_ok(m);
+  }
+  static int64_t pitch4(int64_t n) { return (n + 3) / 4 * 4; }  // 16-byte fp32 rows (TMA)
+
+  // Copy of a rank-4 view into fresh storage whose last `merge` dims form dense rows padded to
+  // 16 bytes: returns the copy with the original shape (pre class, before the op's compute).
+  StridedView padded_copy(const StridedView& v, int merge, const std::string& op) {
+    if (!o_pre.descs.empty() && o_pre_op != op) flush();
+    o_pre_op = op;
+    int64_t inner = 1;
+    for (int i = 4 - merge; i < 4; ++i) inner *= v.shape[i];
+    const int64_t rows = v.elements() / std::max<int64_t>(inner, 1), ld = pitch4(inner);
+    StridedView t = v;
+    t.ptr = alloc_bytes(size_t(rows * ld) * 4);
+    int64_t st = 1;
+    for (int i = 3; i >= 0; --i) {
+      t.st[i] = st;
+      st *= v.shape[i];
+      if (i == 4 - merge) st = ld;
+    }
+    o_pre.descs.push_back(nary_desc(NARY_COPY, t, {v}));
+    return t;
+  }
+
+  // Convolution sub-op on the tensor cores (run_conv, proj/src/dense.cpp:92-157):
+  //   forward      out[n,o,:,:]  = Kmat[o, cuv] . im2col(a)[n][yx, cuv]^T    per image
+  //   grad_weight  gk[o, cuv]    = Gp[o, (n,yx)] . im2col(a)[cuv, (n,yx)]^T  one GEMM
+  //   grad_input   dcol[n][yx,cuv] = G_n^T . Kmat, then col2im (ordered tap sum)
+  // The im2col / permute copies run in the pre class, col2im in the post class.  Every scratch
+  // matrix has 16-byte rows (TMA); padding columns lie outside the tensor maps.
+  void lower_conv_gemm(int ni, const OpSpec& op) {
+    const PlanNode& n = pl.nodes[size_t(ni)];
+    for (int s : n.sources) need(s, C_COMPUTE);
+    if (o_kind >= 0 && (o_kind != 0 || o_op != op.id)) flush();
+    if (!o_pre.descs.empty() && o_pre_op != op.id) flush();
+    if (o_kind < 0) {
+      o_kind = 0;
+      o_op = op.id;
+      prog.gemm_specs.emplace_back();
+      gemm_step.push_back(-1);
+      o_gemm = int(prog.gemm_specs.size()) - 1;
+    }
+    o_pre_op = op.id;
+    const StridedView out = alloc(n.region.shape());
+    set_val(ni, out);
+    const StridedView a = value(n.sources[0]);
+    const StridedView b = value(n.sources[1]);
+    if (a.rank != 4 || b.rank != 4) fail("op '" + op.id + "': conv operands must be rank 4");
+    auto im2col = [&](const StridedView& act, int64_t U, int64_t V, int64_t Yo, int64_t Xo, bool rows,
+                      int64_t& pitch) {
+      const int64_t NB = act.shape[0], K = act.shape[1] * U * V;
+      pitch = rows ? pitch4(K) : pitch4(NB * Yo * Xo);
+      float* t = alloc_bytes(size_t((rows ? NB * Yo * Xo : K) * pitch) * 4);
+      ConvDesc d;
+      std::memset(&d, 0, sizeof d);
+      d.mode = rows ? CONV_IM2COL_ROWS : CONV_IM2COL_COLS;
+      d.a = act;
+      d.out = t;
+      d.n = NB * Yo * Xo * K;
+      d.p[0] = U; d.p[1] = V; d.p[2] = Yo; d.p[3] = Xo; d.p[4] = pitch;
+      o_prec.descs.push_back(d);
+      return t;
+    };
+    auto filter = [&](const StridedView& k) {
+      MatView m;
+      if (filter_mat(k, m)) return m;
+      const StridedView c = padded_copy(k, 3, op.id);
+      m.ptr = c.ptr;
+      m.rows = c.shape[0];
+      m.cols = c.shape[1] * c.shape[2] * c.shape[3];
+      m.rs = c.st[0];
+      m.cs = 1;
+      return m;
+    };
+    auto& specs = prog.gemm_specs[size_t(o_gemm)];
+    double flops = 0;
+    if (op.mode == ConvMode::forward) {
+      const int64_t NB = a.shape[0], C = a.shape[1], O = b.shape[0], U = b.shape[2], V = b.shape[3];
+      const int64_t Yo = out.shape[2], Xo = out.shape[3], K = C * U * V, YX = Yo * Xo;
+      int64_t ld = 0;
+      float* col = im2col(a, U, V, Yo, Xo, true, ld);
+      const MatView km = filter(b);
+      for (int64_t i = 0; i < NB; ++i) {
+        GemmSpec s;
+        s.a = km;
+        s.b = MatView{col + i * YX * ld, YX, K, ld, 1};
+        s.tb = true;
+        s.c = out.ptr + i * O * YX;
+        s.c_rs = YX;
+        specs.push_back(s);
+      }
+      flops = 2.0 * double(NB) * double(O) * double(YX) * double(K);
+    } else if (op.mode == ConvMode::grad_weight) {
+      const int64_t NB = a.shape[0], C = a.shape[1], O = b.shape[1], Yo = b.shape[2], Xo = b.shape[3];
+      const int64_t U = out.shape[2], V = out.shape[3], K = C * U * V, YX = Yo * Xo;
+      int64_t ld = 0;
+      float* col = im2col(a, U, V, Yo, Xo, false, ld);  // [cuv][(n, yx)]
+      // G[n, o, y, x] -> Gp[o][(n, y, x)] (rows padded to 16 bytes)
+      if (!o_pre.descs.empty() && o_pre_op != op.id) flush();
+      o_pre_op = op.id;
+      float* gp = alloc_bytes(size_t(O * ld) * 4);
+      StridedView src = b, dst = b;
+      src.shape[0] = O; src.shape[1] = NB;  // permuted view of G: (o, n, y, x)
+      src.st[0] = b.st[1]; src.st[1] = b.st[0];
+      dst.ptr = gp;
+      dst.shape[0] = O; dst.shape[1] = NB;
+      dst.st[0] = ld; dst.st[1] = YX; dst.st[2] = Xo; dst.st[3] = 1;
+      o_pre.descs.push_back(nary_desc(NARY_COPY, dst, {src}));
+      GemmSpec s;
+      s.a = MatView{gp, O, NB * YX, ld, 1};
+      s.b = MatView{col, K, NB * YX, ld, 1};
+      s.tb = true;
+      s.c = out.ptr;
+      s.c_rs = K;
+      specs.push_back(s);
+      flops = 2.0 * double(O) * double(K) * double(NB * YX);
+    } else {
+      const int64_t NB = a.shape[0], O = a.shape[1], Yo = a.shape[2], Xo = a.shape[3];
+      const int64_t C = b.shape[1], U = b.shape[2], V = b.shape[3], K = C * U * V, YX = Yo * Xo;
+      const MatView km = filter(b);
+      StridedView g = a;
+      if (!(g.st[3] == 1 && g.st[2] == Xo && g.st[1] % 4 == 0 && g.st[0] % 4 == 0 &&
+            (reinterpret_cast<uintptr_t>(g.ptr) & 15) == 0))
+        g = padded_copy(a, 2, op.id);
+      const int64_t ld = pitch4(K);
+      float* dcol = alloc_bytes(size_t(NB * YX * ld) * 4);
+      for (int64_t i = 0; i < NB; ++i) {
+        GemmSpec s;
+        s.a = MatView{g.ptr + i * g.st[0], O, YX, g.st[1], 1};  // G_n [o, yx], used transposed
+        s.ta = true;
+        s.b = km;                                                // Kmat [o, cuv]
+        s.c = dcol + i * YX * ld;
+        s.c_rs = ld;
+        specs.push_back(s);
+      }
+      ConvDesc d;
+      std::memset(&d, 0, sizeof d);
+      d.mode = CONV_COL2IM;
+      d.a.ptr = dcol;
+      d.out = out.ptr;
+      d.n = out.elements();
+      d.p[0] = C; d.p[1] = U; d.p[2] = V; d.p[3] = Yo; d.p[4] = Xo; d.p[5] = ld;
+      o_post.descs.push_back(d);
+      flops = 2.0 * double(NB) * double(YX) * double(K) * double(O);
+    }
+    P.gemm_flops += flops;
+    produced(ni, op.mode == ConvMode::grad_input ? C_POST : C_COMPUTE);
   }
 
   StridedView materialize(int node, const std::string& op) {

@@ -28,6 +28,7 @@ PREC_TF32 = 0
 PREC_FP32 = 1
 FLAG_FUSE = 1
 FLAG_FORCE_XCHG = 2
+FLAG_DIRECT_CONV = 4  # convolutions as direct CUDA-core loops (cross-check of the tcgen05 lowering)
 
 
 @dataclass

@@ -83,13 +83,30 @@ def test_single_rank_lowering_bytes(stem):
 
 
 def _is_mm(P, n):
-    return {o["id"]: o for o in P["graph"]["ops"]}[n["op"]]["kind"] == "matmul"
+    """Sub-ops that run as tcgen05 GEMMs: matmuls, and convolutions (im2col + GEMM)."""
+    return {o["id"]: o for o in P["graph"]["ops"]}[n["op"]]["kind"] in ("matmul", "conv")
+
+
+def _ext(region):
+    return [hi - lo for lo, hi in region]
 
 
 def _mm_flops(P, n):
+    """Multiply-adds of the sub-op's GEMM formulation (csrc/runtime.cpp lower_conv_gemm for
+    convolutions: forward N*O*Yo*Xo*C*U*V, grad_weight O*C*U*V*N*Yo*Xo, grad_input
+    N*Yo*Xo*C*U*V*O with (Yo, Xo) the gradient's extent)."""
     ops = {o["id"]: o for o in P["graph"]["ops"]}
     nodes = {m["id"]: m for m in P["nodes"]}
     op = ops[n["op"]]
+    if op["kind"] == "conv":
+        a, b, o = (_ext(nodes[n["sources"][0]]["region"]), _ext(nodes[n["sources"][1]]["region"]),
+                   _ext(n["region"]))
+        mode = op["attrs"]["mode"]
+        if mode == "forward":
+            return o[0] * o[1] * o[2] * o[3] * b[1] * b[2] * b[3]
+        if mode == "grad_weight":
+            return o[0] * o[1] * o[2] * o[3] * a[0] * b[2] * b[3]
+        return a[0] * a[2] * a[3] * b[1] * b[2] * b[3] * a[1]
     a = nodes[n["sources"][0]]["region"]
     kk = (a[0][1] - a[0][0]) if op["attrs"].get("transpose_a") else (a[1][1] - a[1][0])
     out = n["region"]

@@ -202,3 +202,31 @@ def test_bad_plan_fails_loudly(ctx):
     bad["nodes"] = bad["nodes"][:-1]
     with pytest.raises(TpxError):
         PlanExecutor(ctx, json.dumps(bad))
+
+
+@pytest.mark.parametrize("stem", [s for s in STEMS if s.startswith("cnn")][::2], ids=stem_id)
+def test_tensor_core_conv_matches_direct(ctx, stem):
+    """Convolutions lowered to im2col + tcgen05 GEMM (+ col2im) against the direct CUDA-core
+    loops (TPX_FLAG_DIRECT_CONV), both fp32-accurate (3xTF32 / fp32 FMA), per op on the
+    oracle's inputs: normwise <= 1e-5 on every conv output holder."""
+    from paper_1805_04170_b200.executor import FLAG_DIRECT_CONV, PlanExecutor
+    text, P, seed, _, vals = oracle_values(stem)
+    tc = PlanExecutor(ctx, text, precision=1, flags=0)
+    dc = PlanExecutor(ctx, text, precision=1, flags=FLAG_DIRECT_CONV)
+    assert tc.stats()["n_gemm_launches"] > dc.stats()["n_gemm_launches"]
+    for op in P["graph"]["ops"]:
+        if op["kind"] != "conv":
+            continue
+        outs = []
+        for ex in (tc, dc):
+            ex.init_inputs(seed)
+            for t in op["inputs"]:
+                for hid in P["holders"][t]:
+                    ex.write_node(hid, vals[hid])
+            ex.execute_op(op["id"])
+            ex.synchronize()
+            outs.append({h: ex.read_node(h) for h in P["holders"][op["output"]]})
+        for h in outs[0]:
+            assert normwise(outs[0][h], outs[1][h]) <= 1e-5, (op["id"], h)
+    tc.close()
+    dc.close()
