@@ -37,6 +37,14 @@ CONFIGS = {
     "alexfc_b128": {"batch": 128, "dims": [9216, 4096, 4096, 1000], "sample": "alexfc_layer_sample_b1"},
     "vggfc_b64": {"batch": 64, "dims": [25088, 4096, 4096, 1000], "sample": "vggfc_layer_sample_b1"},
     "cfg5_mlp3x32768_b32": {"batch": 32, "dims": [32768] * 4, "sample": "cfg5_layer_sample_b1"},
+    "alexconv_b128": {"batch": 128, "conv": True, "sample": "alexconv_layer_sample_b1"},
+    "vggconv_b64": {"batch": 64, "conv": True, "sample": "vggconv_layer_sample_b1"},
+}
+# Whole AlexNet-/VGG-style networks: the conv component and the FC component are planned
+# separately (the IR has no flatten, SURVEY finding 7) and a train step executes both plans.
+NETWORKS = {
+    "alexnet_b128": ["alexconv_b128", "alexfc_b128"],   # BASELINE configs[2]
+    "vgg_b64": ["vggconv_b64", "vggfc_b64"],            # BASELINE configs[3]
 }
 METRIC = "samples/sec per train step, optimal tiling vs data-parallel, at 1/2/4/8 B200"
 SEED = 7
@@ -47,6 +55,9 @@ def load_plan(name, mode, k):
 
 
 def graph_flops(graph):
+    """Algorithmic FLOPs of one step of `graph`: 2*M*N*K per matmul plus 2*|out|*contraction per
+    convolution; elementwise ops are not counted."""
+    from paper_1805_04170_b200.graphs import conv_flops
     shapes = {t["id"]: t["shape"] for t in graph["tensors"]}
     f = 0
     for op in graph["ops"]:
@@ -55,7 +66,37 @@ def graph_flops(graph):
             kk = a[0] if op["attrs"].get("transpose_a") else a[1]
             o = shapes[op["output"]]
             f += 2 * o[0] * o[1] * kk
-    return f
+    return f + conv_flops(json.dumps(graph))
+
+
+def parts_of(workload):
+    return NETWORKS.get(workload, [workload])
+
+
+def workload_batch(workload):
+    return CONFIGS[parts_of(workload)[0]]["batch"]
+
+
+def workload_config(workload, k):
+    """The JSON line's `config` object."""
+    parts = parts_of(workload)
+    c = {"workload": workload, "global_batch": workload_batch(workload), "plan": f"kcuts optimal k={k}",
+         "parallelism": f"tiled{1 << k}", "l2": "inputs > L2 (weights or im2col operands > 126 MB per step); no flush"}
+    if len(parts) > 1 or CONFIGS[parts[0]].get("conv"):
+        c["components"] = {}
+        for p in parts:
+            g = json.loads(load_plan(p, "opt", 0))["graph"]
+            convs = [o for o in g["ops"] if o["kind"] == "conv" and o["attrs"]["mode"] == "forward"]
+            sh = {t["id"]: t["shape"] for t in g["tensors"]}
+            if convs:
+                c["components"][p] = {"input": sh["a0"], "filters": [sh[o["inputs"][1]] for o in convs],
+                                      "stride": 1, "padding": "valid"}
+            else:
+                c["components"][p] = {"fc_dims": CONFIGS[p]["dims"]}
+    else:
+        d = CONFIGS[parts[0]]["dims"]
+        c.update({"hidden": d[1], "layers": len(d) - 1})
+    return c
 
 
 def peaks():
@@ -110,49 +151,51 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_pool(cfg, threads):
+def cpu_pools(workload, threads):
     """The reference's CPU tiled executor (execute_numeric's node loop through the reference
-    library compiled from its own sources, oracle/_ref) on a bounded sample of the workload:
-    ONE sample through ONE layer of the config's width, `threads` independent copies (the
-    reference is single-threaded).  A step's samples/s = threads / wall / ratio, where ratio =
-    full per-sample FLOPs / layer-sample FLOPs."""
+    library compiled from its own sources, oracle/_ref) on a bounded sample of each component:
+    ONE sample through ONE layer (a train step of that layer), `threads` independent copies
+    (the reference is single-threaded).  Per component, ratio = the component's per-sample
+    FLOPs / the layer sample's FLOPs; a sample of the workload costs sum(secs x ratio)."""
     from oracle import ref
-    text = load_plan(cfg["sample"], "opt", 0)
-    ratio = (full_flops(cfg) / cfg["batch"]) / graph_flops(json.loads(text)["graph"])
-    return ref.Pool(text, SEED, threads), ratio
-
-
-def full_flops(cfg):
-    b, d = cfg["batch"], cfg["dims"]
-    # gen_mlp train step: per layer fwd + bwd_w + bwd_x, each 2*b*d_in*d_out
-    return sum(3 * 2 * b * d[i] * d[i + 1] for i in range(len(d) - 1))
+    out = []
+    for p in parts_of(workload):
+        cfg = CONFIGS[p]
+        text = load_plan(cfg["sample"], "opt", 0)
+        full = graph_flops(json.loads(load_plan(p, "opt", 0))["graph"]) / cfg["batch"]
+        ratio = full / graph_flops(json.loads(text)["graph"])
+        out.append((p, ref.Pool(text, SEED, threads), ratio))
+    return out
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
     import psutil
     cores = os.cpu_count() or 1
-    per_run = 6 * 2 ** 30 * (cfg["dims"][1] / 8192) ** 2
+    widths = [CONFIGS[p]["dims"][1] if "dims" in CONFIGS[p] else 4096 for p in parts_of(args.config)]
+    per_run = 6 * 2 ** 30 * (max(widths) / 8192) ** 2
     threads = max(1, min(cores, int(psutil.virtual_memory().available * 0.5 // per_run), 64))
-    pool, ratio = cpu_pool(cfg, threads)
+    pools = cpu_pools(args.config, threads)
     thr = threads
-    for _ in range(min(args.warmup, 1)):  # CPU path: one untimed pass warms caches/allocator
-        pool.step()
-    secs = [pool.step() for _ in range(args.steps)]
-    pool.close()
-    v = thr * len(secs) / (sum(secs) * ratio)
+    for _, pool, _ in pools:  # CPU path: one untimed pass warms caches/allocator
+        if args.warmup:
+            pool.step()
+    per_sample = []  # seconds of one workload sample, per step
+    for _ in range(args.steps):
+        per_sample.append(sum(pool.step() * ratio for _, pool, ratio in pools) / thr)
+    for _, pool, _ in pools:
+        pool.close()
+    v = len(per_sample) / sum(per_sample)
     sample = (f"{thr} concurrent copies of the reference's tiled node loop (execute_numeric semantics, "
-              f"fp64, single-threaded each) on one sample through one {cfg['dims'][1]}-wide layer of "
-              f"{args.config} per step ({statistics.mean(secs):.2f} s/step); samples/s = copies x steps / "
-              f"wall / {ratio:.3g} (FLOP ratio full sample : layer sample); {min(args.warmup, 1)} warm-up pass")
+              f"fp64, single-threaded each) on one sample through one layer of each component "
+              f"({', '.join(f'{p} x{r:.3g}' for p, _, r in pools)}: FLOP ratio full sample : layer sample) per "
+              f"step; samples/s = copies / sum(layer-sample wall x ratio); 1 warm-up pass")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.config, "global_batch": cfg["batch"],
-                                        "hidden": cfg["dims"][1], "layers": len(cfg["dims"]) - 1},
+        "data": "synthetic", "config": workload_config(args.config, int(round(math.log2(max(args.gpus, 1))))),
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": thr, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -171,7 +214,7 @@ def kernel_rooflines(r, tensor_peak, hbm_peak):
     for st, ms in zip(r["steps_desc"], r["step_ms"]):
         if st["kind"] != "gemm":
             continue
-        name = re.sub(r"\d+$", "", st["op"])
+        name = (st["part"] + ":" if st.get("part") else "") + re.sub(r"\d+$", "", st["op"])
         c = cls.setdefault(name, {"class": name, "launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0,
                                   "what": f"{'T' if st['ta'] else 'N'}{'T' if st['tb'] else 'N'} "
                                           f"{'x'.join(str(v) for v in st['shapes'][0][:3])}, "
@@ -233,7 +276,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2_mlp5x8192_b512", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg2_mlp5x8192_b512", choices=sorted(CONFIGS) + sorted(NETWORKS))
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -269,7 +312,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
-    cfg = CONFIGS[args.config]
+    parts = parts_of(args.config)
+    batch = workload_batch(args.config)
     prec = 0 if args.precision == "tf32" else 1
     ctx = Context(local, rank, world)
     if world > 1:
@@ -278,51 +322,80 @@ def main():
     hbm_peak, bf16_peak, peak_kind = peaks()
     res = {}
     for mode in ("opt", "data"):
-        text = load_plan(args.config, mode, k)
-        ex = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE)
-        ex.set_stream(stream.cuda_stream)
-        st = ex.stats()
-        ex.init_inputs(SEED)
+        exs, texts = [], []
+        for part in parts:
+            text = load_plan(part, mode, k)
+            ex = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE)
+            ex.set_stream(stream.cuda_stream)
+            ex.init_inputs(SEED)
+            exs.append(ex)
+            texts.append(text)
+        sts = [ex.stats() for ex in exs]
+        st = {key: sum(x[key] for x in sts) for key in sts[0]}
+
+        def step():
+            for ex in exs:
+                ex.execute()
+
         for _ in range(args.warmup):
-            ex.execute()
+            step()
         clk = ClockSampler(local)
         with clk:
-            ms = timed(ex.execute, stream, args.steps, barrier)
+            ms = timed(step, stream, args.steps, barrier)
         ms = max_over_ranks(ms)
-        r = {"ms_per_step": ms / args.steps, "value": cfg["batch"] * args.steps / (ms / 1e3),
+        r = {"ms_per_step": ms / args.steps, "value": batch * args.steps / (ms / 1e3),
              "stats": st, "clocks": clk.summary()}
         # per-launch timing pass (events between every lowered step) for the roofline
-        ex.enable_timing(True)
-        g_ms, t_ms, per_step = [], [], []
+        g_ms, t_ms, per_step, desc = [], [], [], []
+        for ex, part in zip(exs, parts):
+            ex.enable_timing(True)
+            desc += [dict(d, part=part if len(parts) > 1 else "") for d in ex.describe()["main"]["steps"]]
         for _ in range(5):
-            ex.execute()
-            t = ex.last_timing()
-            g_ms.append(t["gemm_ms"])
-            t_ms.append(t["total_ms"])
-            per_step.append(ex.last_step_times())
-        ex.enable_timing(False)
+            g = t = 0.0
+            ps = []
+            for ex in exs:
+                ex.execute()
+                tt = ex.last_timing()
+                g += tt["gemm_ms"]
+                t += tt["total_ms"]
+                ps += ex.last_step_times()
+            g_ms.append(g)
+            t_ms.append(t)
+            per_step.append(ps)
+        for ex in exs:
+            ex.enable_timing(False)
         r["gemm_ms"] = statistics.median(g_ms)
         r["timed_total_ms"] = statistics.median(t_ms)
         r["step_ms"] = [statistics.median(x) for x in zip(*per_step)]
-        r["steps_desc"] = ex.describe()["main"]["steps"]
-        # e2e through the public API: host (pinned) x0 in, network output out, every step
-        plan = json.loads(text)
-        mine = set(ex.my_devices())
-        nodes = {n["id"]: n for n in plan["nodes"]}
-        last = f"x{len(cfg['dims']) - 1}"
-        ins = [h for h in plan["holders"]["x0"] if nodes[h]["device"] in mine]
-        outs = [h for h in plan["holders"][last] if nodes[h]["device"] in mine]
-        hin = {h: torch.empty(math.prod(ex.node_shape(h)), dtype=torch.float32, pin_memory=True).uniform_(-1, 1)
-               for h in ins}
-        hout = {h: torch.empty(math.prod(ex.node_shape(h)), dtype=torch.float32, pin_memory=True) for h in outs}
-        h2d = sum(v.numel() * 4 for v in hin.values())
-        d2h = sum(v.numel() * 4 for v in hout.values())
+        r["steps_desc"] = desc
+        # e2e through the public API: every component's graph input (x0 / a0) from pinned host
+        # memory in, the component's network output (the seed op's input) out, every step
+        hin, hout = [], []
+        for ex, text in zip(exs, texts):
+            plan = json.loads(text)
+            mine = set(ex.my_devices())
+            nodes = {n["id"]: n for n in plan["nodes"]}
+            roles = {t["id"]: t["role"] for t in plan["graph"]["tensors"]}
+            src = [t for t, rl in roles.items() if rl == "input"]
+            last = next(o["inputs"][0] for o in plan["graph"]["ops"] if o["id"] == "seed")
+            for t in src:
+                for h in plan["holders"][t]:
+                    if nodes[h]["device"] in mine:
+                        hin.append((ex, h, torch.empty(math.prod(ex.node_shape(h)), dtype=torch.float32,
+                                                       pin_memory=True).uniform_(-1, 1)))
+            for h in plan["holders"][last]:
+                if nodes[h]["device"] in mine:
+                    hout.append((ex, h, torch.empty(math.prod(ex.node_shape(h)), dtype=torch.float32,
+                                                    pin_memory=True)))
+        h2d = sum(v.numel() * 4 for _, _, v in hin)
+        d2h = sum(v.numel() * 4 for _, _, v in hout)
 
         def e2e_step():
-            for h, v in hin.items():
+            for ex, h, v in hin:
                 ex.write_node_f32_from(h, v.data_ptr(), v.numel())
-            ex.execute()
-            for h, v in hout.items():
+            for ex in exs:
+                ex.execute()
+            for ex, h, v in hout:
                 ex.read_node_f32_into(h, v.data_ptr(), v.numel())
 
         for _ in range(2):
@@ -331,22 +404,24 @@ def main():
         tot = torch.tensor([h2d, d2h], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(tot)
-        r["e2e"] = {"value": cfg["batch"] * args.steps / (e_ms / 1e3), "unit": "samples/s",
+        r["e2e"] = {"value": batch * args.steps / (e_ms / 1e3), "unit": "samples/s",
                     "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item())}
         res[mode] = r
-        ex.close()
+        for ex in exs:
+            ex.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            pool, ratio = cpu_pool(cfg, 1)
-            secs = pool.step()
-            pool.close()
-            cpu = {"value": 1.0 / (secs * ratio), "unit": "samples/s", "cores": 1, "kind": "reference",
+            pools = cpu_pools(args.config, 1)
+            secs = sum(pool.step() * ratio for _, pool, ratio in pools)
+            for _, pool, _ in pools:
+                pool.close()
+            cpu = {"value": 1.0 / secs, "unit": "samples/s", "cores": 1, "kind": "reference",
                    "sample": (f"reference tiled node loop (execute_numeric semantics; oracle/_ref built from "
-                              f"the reference's sources; fp64, 1 thread) on 1 sample through 1 "
-                              f"{cfg['dims'][1]}-wide layer of {args.config}: {secs:.2f} s; scaled by the "
-                              f"FLOP ratio {ratio:.3g} (full sample : layer sample)")}
+                              f"the reference's sources; fp64, 1 thread) on 1 sample through 1 layer of each "
+                              f"component of {args.config}, scaled by the FLOP ratio full sample : layer sample "
+                              f"({', '.join(f'{p} x{r:.3g}' for p, _, r in pools)}): {secs:.2f} s per sample")}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -364,9 +439,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": o["ms_per_step"],
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "tf32" if prec == 0 else "fp32(3xtf32)", "data": "synthetic",
-        "config": {"workload": args.config, "global_batch": cfg["batch"], "hidden": cfg["dims"][1],
-                   "layers": len(cfg["dims"]) - 1, "plan": f"kcuts optimal k={k}",
-                   "parallelism": f"tiled{world}", "l2": "inputs > L2 (weights 1.34 GB/step); no flush"},
+        "config": workload_config(args.config, k),
         "dp": {"value": d["value"], "ms_per_step": d["ms_per_step"], "plan": f"preset data k={k}",
                "e2e": d["e2e"]["value"], "fetch_bytes_total": d["stats"]["fetch_bytes_total"]},
         "opt_vs_dp": o["value"] / d["value"],

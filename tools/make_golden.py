@@ -29,7 +29,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from oracle import ref  # noqa: E402
+from oracle import ref
+from paper_1805_04170_b200 import graphs as G  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 SMALL = 50_000
@@ -66,6 +67,8 @@ def graphs() -> dict:
     g["cfg5r_mlp3x512_b32"] = ref.gen_mlp(32, [512] * 4)      # configs[4] structure, reduced
     g["fcr_alexnet_b32"] = ref.gen_mlp(32, [576, 256, 256, 64])  # AlexNet FC6-8 structure
     g["cnnr_train_b16"] = ref.gen_cnn(16, (10, 10), [4, 8, 8], (3, 3), backward=True)
+    # AlexNet-style conv component (per-layer filters + SGD update; paper_1805_04170_b200/graphs.py)
+    g["alexr_conv_b4"] = G.conv_net(4, (16, 16), [3, 8, 16, 8], [(5, 5), (3, 3), (3, 3)])
     g["reduce_kat"] = reduce_kat_graph()
     return g
 
@@ -94,6 +97,11 @@ def cases():
         out.append(("cnnr_train_b16", "opt", k, 7))
     for k in (1, 2):
         out.append(("cnnr_train_b16", "data", k, 7))
+    for k in (0, 1, 2):
+        out.append(("alexr_conv_b4", "opt", k, 7))
+    for k in (1, 2):
+        out.append(("alexr_conv_b4", "data", k, 7))
+    out.append(("alexr_conv_b4", "model", 2, 7))
     out.append(("reduce_kat", "custom", 1, 5))
     return out
 

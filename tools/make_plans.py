@@ -18,6 +18,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle import ref  # noqa: E402
+from paper_1805_04170_b200 import graphs as G  # noqa: E402
 
 OUT = os.path.join(ROOT, "plans")
 
@@ -30,6 +31,11 @@ CONFIGS = {
     "vggfc_b64": (64, [25088, 4096, 4096, 1000]),     # configs[3] FC component
     "cfg5_mlp3x32768_b32": (32, [32768] * 4),        # configs[4] wide-FC stress
 }
+# Conv components of the AlexNet-/VGG-style configs (graphs.py; the FC components are above).
+CONV_CONFIGS = {
+    "alexconv_b128": lambda: G.alexnet_conv(128),   # configs[2] conv component
+    "vggconv_b64": lambda: G.vgg_conv(64),          # configs[3] conv component
+}
 # Bounded CPU samples of each config for the reference's CPU executor (bench.py cpu_baseline
 # and --impl reference): one sample through one layer (fwd, act, seed, bwd_w, bwd_x, step,
 # upd) of the same width; a full sample is layers x this.
@@ -40,27 +46,37 @@ SAMPLES = {
     "vggfc_b64": ("vggfc_layer_sample_b1", 1, [4096, 4096], 3),
     "cfg5_mlp3x32768_b32": ("cfg5_layer_sample_b1", 1, [32768, 32768], 3),
 }
+# conv samples: one image through the component's heaviest layer (train step of that layer)
+CONV_SAMPLES = {
+    "alexconv_b128": ("alexconv_layer_sample_b1", lambda: G.conv_net(1, (32, 32), [384, 384], [(3, 3)])),
+    "vggconv_b64": ("vggconv_layer_sample_b1", lambda: G.conv_net(1, (11, 11), [512, 512], [(3, 3)])),
+}
+
+
+def write(path, text):
+    with gzip.GzipFile(path, "wb", mtime=0) as f:
+        f.write(text.encode())
 
 
 def main():
     os.makedirs(OUT, exist_ok=True)
-    names = sys.argv[1:] or list(CONFIGS)
+    names = sys.argv[1:] or list(CONFIGS) + list(CONV_CONFIGS)
     for name in names:
-        batch, dims = CONFIGS[name]
-        g = ref.gen_mlp(batch, dims)
+        g = CONV_CONFIGS[name]() if name in CONV_CONFIGS else ref.gen_mlp(*CONFIGS[name])
         for mode in ("opt", "data"):
             for k in range(4):
                 text = ref.plan(g, mode, k)
                 P = json.loads(text)
                 path = os.path.join(OUT, f"{name}.{mode}.k{k}.plan.json.gz")
-                with gzip.GzipFile(path, "wb", mtime=0) as f:
-                    f.write(text.encode())
+                write(path, text)
                 print(f"{os.path.basename(path)}: {len(P['nodes'])} nodes, "
                       f"fetch_bytes_total {P['fetch_bytes_total']}")
-        sname, sb, sdims, _ = SAMPLES[name]
-        text = ref.plan(ref.gen_mlp(sb, sdims), "opt", 0)
-        with gzip.GzipFile(os.path.join(OUT, f"{sname}.opt.k0.plan.json.gz"), "wb", mtime=0) as f:
-            f.write(text.encode())
+        if name in CONV_SAMPLES:
+            sname, gen = CONV_SAMPLES[name]
+            write(os.path.join(OUT, f"{sname}.opt.k0.plan.json.gz"), ref.plan(gen(), "opt", 0))
+        else:
+            sname, sb, sdims, _ = SAMPLES[name]
+            write(os.path.join(OUT, f"{sname}.opt.k0.plan.json.gz"), ref.plan(ref.gen_mlp(sb, sdims), "opt", 0))
 
 
 if __name__ == "__main__":
