@@ -85,8 +85,11 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
   const int64_t rb = local / D.n_col_chunks, cc = local % D.n_col_chunks;
   const int64_t r0 = rb * D.rpt, r1 = min(D.rows, r0 + D.rpt);
   const int64_t c0 = cc * D.col_chunk, c1 = min(D.inner, c0 + D.col_chunk);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nin = d.nin, op = d.op;
+  // one row per warp; a block holding a single (long) row spreads it over all its threads
+  const bool one = (r1 - r0) == 1;
+  const int warp = one ? 0 : int(threadIdx.x >> 5), lane = one ? int(threadIdx.x) : int(threadIdx.x & 31);
+  const int cstep = one ? kThreads : 32;
   for (int64_t r = r0 + warp; r < r1; r += kThreads / 32) {
     const int64_t i2 = r % d.shape[2];
     const int64_t t = r / d.shape[2];
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
     for (int k = 0; k < kMaxIn; ++k)
       if (k < nin) in[k] = d.in[k] + i0 * d.in_st[k][0] + i1 * d.in_st[k][1] + i2 * d.in_st[k][2];
     if (d.vec == 4) {
-      for (int64_t c = c0 + lane; c < c1; c += 32) {
+      for (int64_t c = c0 + lane; c < c1; c += cstep) {
         float4 v[kMaxIn];
 #pragma unroll
         for (int k = 0; k < kMaxIn; ++k)
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
       }
     } else {
       const int64_t os = d.out_st[3];
-      for (int64_t c = c0 + lane; c < c1; c += 32) {
+      for (int64_t c = c0 + lane; c < c1; c += cstep) {
         float a[kMaxIn];
 #pragma unroll
         for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? __ldg(in[k] + c * d.in_st[k][3]) : 0.f;
@@ -188,53 +191,6 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restri
   const ConvDesc& d = ds[di];
   const int64_t e = (int64_t(blockIdx.x) - d.tile_begin) * kThreads + threadIdx.x;
   if (e >= d.n) return;
-  if (d.mode >= CONV_IM2COL_ROWS) {
-    // data movement of the tensor-core conv lowering; consecutive threads write consecutive
-    // output elements (coalesced stores), the gathers hit L1/L2 (each input element is read
-    // U*V times by neighbouring threads)
-    if (d.mode == CONV_COL2IM) {
-      const int64_t C = d.p[0], U = d.p[1], V = d.p[2], Yo = d.p[3], Xo = d.p[4], pitch = d.p[5];
-      const int64_t H = Yo + U - 1, W = Xo + V - 1;
-      const int64_t x = e % W;
-      int64_t t = e / W;
-      const int64_t y = t % H;
-      t /= H;
-      const int64_t c = t % C;
-      const int64_t nb = t / C;
-      const float* col = d.a.ptr + nb * (Yo * Xo * pitch);
-      float acc = 0.f;
-      for (int64_t u = 0; u < U; ++u) {
-        const int64_t yy = y - u;
-        if (yy < 0 || yy >= Yo) continue;
-        for (int64_t v = 0; v < V; ++v) {
-          const int64_t xx = x - v;
-          if (xx < 0 || xx >= Xo) continue;
-          acc += __ldg(col + (yy * Xo + xx) * pitch + (c * U + u) * V + v);
-        }
-      }
-      d.out[e] = acc;
-      return;
-    }
-    const int64_t U = d.p[0], V = d.p[1], Yo = d.p[2], Xo = d.p[3], pitch = d.p[4];
-    const int64_t C = d.a.shape[1], NB = d.a.shape[0], K = C * U * V, YX = Yo * Xo;
-    int64_t nb, yx, k, dst;
-    if (d.mode == CONV_IM2COL_ROWS) {
-      k = e % K;
-      const int64_t r = e / K;
-      yx = r % YX;
-      nb = r / YX;
-      dst = r * pitch + k;
-    } else {
-      const int64_t m = e % (NB * YX);
-      k = e / (NB * YX);
-      yx = m % YX;
-      nb = m / YX;
-      dst = k * pitch + m;
-    }
-    const int64_t v = k % V, u = (k / V) % U, c = k / (U * V);
-    d.out[dst] = at4(d.a, nb, c, yx / Xo + u, yx % Xo + v);
-    return;
-  }
   const int64_t o3 = e % d.oshape[3];
   int64_t t = e / d.oshape[3];
   const int64_t o2 = t % d.oshape[2];
@@ -270,6 +226,82 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restri
       }
   }
   d.out[e] = acc;
+}
+
+// im2col / col2im of the tensor-core conv lowering: one warp per output row (lanes over x), so
+// reads and writes are coalesced and the index decomposition is paid once per row.
+constexpr int kRowsPerWarp = 8;
+
+__global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __restrict__ ds, int n) {
+  const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
+  const ConvDesc& d = ds[di];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kRowsPerBlock = (kThreads / 32) * kRowsPerWarp;
+  const int tile = int(int64_t(blockIdx.x) - d.tile_begin);
+  const int NB = int(d.a.shape[0]);
+  if (d.mode == CONV_IM2COL) {
+    // block = (k, chunk of kRowsPerBlock (nb, y) rows); per row
+    //   out[k*pitch + nb*img + y*Xo + x] = a[nb, c, y+u, x+v]
+    // the index decomposition of k is paid once per block, of (nb, y) once per row (32-bit),
+    // and a warp's rows issue their loads together
+    const int U = int(d.p[0]), V = int(d.p[1]), Yo = int(d.p[2]), Xo = int(d.p[3]);
+    const int64_t pitch = d.p[4], img = d.p[5];
+    const int R = NB * Yo, nblk = (R + kRowsPerBlock - 1) / kRowsPerBlock;
+    const int k = tile / nblk, rb = tile - k * nblk;
+    const int v = k % V, u = (k / V) % U, c = k / (U * V);
+    const float* src0 = d.a.ptr + c * d.a.st[1] + u * d.a.st[2] + v * d.a.st[3];
+    float* dst0 = d.out + int64_t(k) * pitch;
+    const int r0 = rb * kRowsPerBlock + warp * kRowsPerWarp;
+    for (int x0 = 0; x0 < Xo; x0 += 32) {
+      const int x = x0 + lane;
+      float val[kRowsPerWarp];
+      float* dst[kRowsPerWarp];
+#pragma unroll
+      for (int j = 0; j < kRowsPerWarp; ++j) {
+        const int r = r0 + j;
+        dst[j] = nullptr;
+        val[j] = 0.f;
+        if (r < R && x < Xo) {
+          const int nb = r / Yo, y = r - nb * Yo;
+          val[j] = __ldg(src0 + nb * d.a.st[0] + y * d.a.st[2] + x * d.a.st[3]);
+          dst[j] = dst0 + nb * img + y * Xo + x;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kRowsPerWarp; ++j)
+        if (dst[j]) *dst[j] = val[j];
+    }
+  } else {
+    // block = ((nb, c), chunk of kRowsPerBlock y rows); per output element
+    //   out[nb, c, y, x] = sum_{u,v} col[(c,u,v)*pitch + nb*img + (y-u)*Xo + (x-v)]
+    const int C = int(d.p[0]), U = int(d.p[1]), V = int(d.p[2]), Yo = int(d.p[3]), Xo = int(d.p[4]);
+    const int64_t pitch = d.p[5], img = d.p[6];
+    const int H = Yo + U - 1, W = Xo + V - 1;
+    const int nblk = (H + kRowsPerBlock - 1) / kRowsPerBlock;
+    const int nc = tile / nblk, yb = tile - nc * nblk;
+    const int c = nc % C, nb = nc / C;
+    const float* col = d.a.ptr + int64_t(nb) * img + int64_t(c * U * V) * pitch;
+    float* out = d.out + int64_t(nc) * H * W;
+    const int y0 = yb * kRowsPerBlock + warp * kRowsPerWarp;
+    for (int j = 0; j < kRowsPerWarp; ++j) {
+      const int y = y0 + j;
+      if (y >= H) break;
+      for (int x = lane; x < W; x += 32) {
+        float acc = 0.f;
+        for (int u = 0; u < U; ++u) {
+          const int yy = y - u;
+          if (yy < 0 || yy >= Yo) continue;
+          const float* crow = col + int64_t(u * V) * pitch + yy * Xo;
+#pragma unroll 4
+          for (int vv = 0; vv < V; ++vv) {
+            const int xx = x - vv;
+            if (xx >= 0 && xx < Xo) acc += __ldg(crow + int64_t(vv) * pitch + xx);
+          }
+        }
+        out[int64_t(y) * W + x] = acc;
+      }
+    }
+  }
 }
 
 template <class T>
@@ -428,9 +460,22 @@ void init_free(InitBatch& b) {
 
 void conv_prepare(ConvBatch& b) {
   int64_t tiles = 0;
+  b.move = !b.descs.empty() && b.descs[0].mode >= CONV_IM2COL;
   for (auto& d : b.descs) {
+    if ((d.mode >= CONV_IM2COL) != b.move) throw std::runtime_error("conv batch mixes compute and data movement");
     d.tile_begin = tiles;
-    tiles += (d.n + kThreads - 1) / kThreads;
+    if (b.move) {
+      const int64_t rpb = (kThreads / 32) * kRowsPerWarp;
+      if (d.mode == CONV_IM2COL) {  // K x ceil(N*Yo / rpb) blocks
+        const int64_t K = d.a.shape[1] * d.p[0] * d.p[1];
+        tiles += K * ((d.a.shape[0] * d.p[2] + rpb - 1) / rpb);
+      } else {                      // N*C x ceil(H / rpb) blocks
+        const int64_t H = d.p[3] + d.p[1] - 1;
+        tiles += d.a.shape[0] * d.p[0] * ((H + rpb - 1) / rpb);
+      }
+    } else {
+      tiles += (d.n + kThreads - 1) / kThreads;
+    }
   }
   b.tiles = tiles;
   upload(b.descs, &b.d_descs);
@@ -438,8 +483,12 @@ void conv_prepare(ConvBatch& b) {
 
 void conv_run(const ConvBatch& b, cudaStream_t s) {
   if (!b.tiles) return;
-  conv_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const ConvDesc*>(b.d_descs),
-                                                     int(b.descs.size()));
+  if (b.move)
+    convmove_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const ConvDesc*>(b.d_descs),
+                                                           int(b.descs.size()));
+  else
+    conv_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const ConvDesc*>(b.d_descs),
+                                                       int(b.descs.size()));
   CUDA_CHECK(cudaGetLastError());
 }
 

@@ -93,11 +93,13 @@ uint64_t fnv1a(const char* s, size_t n);
 // data-movement kernels of the tensor-core lowering (conv = im2col + tcgen05 GEMM [+ col2im]).
 enum ConvModeCode : int {
   CONV_FWD = 0, CONV_GRAD_W = 1, CONV_GRAD_IN = 2,
-  CONV_IM2COL_ROWS = 3,  // out[(n*Yo*Xo + y*Xo+x)*pitch + c*U*V+u*V+v] = a[n,c,y+u,x+v]
-  CONV_IM2COL_COLS = 4,  // out[(c*U*V+u*V+v)*pitch + n*Yo*Xo + y*Xo+x] = a[n,c,y+u,x+v]
-                         //   (p = U,V,Yo,Xo,pitch; pitch >= the row length, 16-byte rows)
-  CONV_COL2IM = 5,       // out[n,c,y,x] = sum_{u,v} col[(n*Yo*Xo + (y-u)*Xo+(x-v))*pitch + c*U*V+u*V+v]
-                         //   (a.ptr = col, p = C,U,V,Yo,Xo,pitch; taps in ascending (u, v) order)
+  CONV_IM2COL = 4,       // out[(c*U*V+u*V+v)*pitch + n*img + y*Xo+x] = a[n,c,y+u,x+v]
+                         //   (d.n = rows (k, n, y); col2im: d.n = rows (n, c, y))
+                         //   (p = U,V,Yo,Xo,pitch,img; img >= Yo*Xo per-image column stride,
+                         //   pitch >= N*img, 16-byte rows)
+  CONV_COL2IM = 5,       // out[n,c,y,x] = sum_{u,v} col[(c*U*V+u*V+v)*pitch + n*img + (y-u)*Xo+(x-v)]
+                         //   (a.ptr = col, a.shape[0] = N, p = C,U,V,Yo,Xo,pitch,img; taps in
+                         //   ascending (u, v) order)
 };
 struct ConvDesc {
   int mode;
@@ -105,7 +107,7 @@ struct ConvDesc {
   float* out;         // contiguous output
   int64_t oshape[4];
   int64_t n;          // output elements
-  int64_t p[6];       // mode parameters (see ConvModeCode)
+  int64_t p[8];       // mode parameters (see ConvModeCode)
   int64_t tile_begin;
 };
 struct ConvBatch {
@@ -113,6 +115,7 @@ struct ConvBatch {
   void* d_descs = nullptr;
   int64_t tiles = 0;
   double flops = 0;
+  bool move = false;  // im2col / col2im batch (d.n counts rows) rather than direct conv
 };
 void conv_prepare(ConvBatch& b);
 void conv_run(const ConvBatch& b, cudaStream_t s);

@@ -88,6 +88,7 @@ struct Lowerer {
       : P(p), pl(p.plan), C(*p.ctx), prog(pr), dry(d),
         fuse(p.flags & 1), force_xchg(p.flags & 2), tc_conv(!(p.flags & 4)) {}
   bool tc_conv;
+  std::map<std::vector<int64_t>, float*> col_cache;  // im2col buffers by (view, filter) key
 
   float* alloc_bytes(size_t bytes) {
     const size_t off = (P.arena_used + kAlign - 1) / kAlign * kAlign;
@@ -325,18 +326,30 @@ struct Lowerer {
     const StridedView a = value(n.sources[0]);
     const StridedView b = value(n.sources[1]);
     if (a.rank != 4 || b.rank != 4) fail("op '" + op.id + "': conv operands must be rank 4");
-    auto im2col = [&](const StridedView& act, int64_t U, int64_t V, int64_t Yo, int64_t Xo, bool rows,
+    // im2col in the columns layout col[(c,u,v)][(n,y,x)], rows padded to 16 bytes
+    // img = per-image column stride: Yo*Xo (dense, one GEMM over all images) or padded to 16
+    // bytes so that every image's column block can be a TMA operand of its own problem
+    auto im2col = [&](const StridedView& act, int64_t U, int64_t V, int64_t Yo, int64_t Xo, int64_t img,
                       int64_t& pitch) {
       const int64_t NB = act.shape[0], K = act.shape[1] * U * V;
-      pitch = rows ? pitch4(K) : pitch4(NB * Yo * Xo);
-      float* t = alloc_bytes(size_t((rows ? NB * Yo * Xo : K) * pitch) * 4);
+      pitch = pitch4(NB * img);
+      // forward and grad_weight of a layer read the same activation view: one im2col
+      std::vector<int64_t> key = {int64_t(reinterpret_cast<uintptr_t>(act.ptr)), U, V, img};
+      for (int i = 0; i < act.rank; ++i) {
+        key.push_back(act.shape[i]);
+        key.push_back(act.st[i]);
+      }
+      auto hit = col_cache.find(key);
+      if (hit != col_cache.end()) return hit->second;
+      float* t = alloc_bytes(size_t(K * pitch) * 4);  // padding columns stay 0 (zeroed arena)
+      col_cache[key] = t;
       ConvDesc d;
       std::memset(&d, 0, sizeof d);
-      d.mode = rows ? CONV_IM2COL_ROWS : CONV_IM2COL_COLS;
+      d.mode = CONV_IM2COL;
       d.a = act;
       d.out = t;
-      d.n = NB * Yo * Xo * K;
-      d.p[0] = U; d.p[1] = V; d.p[2] = Yo; d.p[3] = Xo; d.p[4] = pitch;
+      d.n = K * NB * Yo;  // rows
+      d.p[0] = U; d.p[1] = V; d.p[2] = Yo; d.p[3] = Xo; d.p[4] = pitch; d.p[5] = img;
       o_prec.descs.push_back(d);
       return t;
     };
@@ -354,27 +367,30 @@ struct Lowerer {
     auto& specs = prog.gemm_specs[size_t(o_gemm)];
     double flops = 0;
     if (op.mode == ConvMode::forward) {
+      // out[n][o][yx] = Kmat[o, cuv] . col[cuv, n*YX + yx]   (one problem per image)
       const int64_t NB = a.shape[0], C = a.shape[1], O = b.shape[0], U = b.shape[2], V = b.shape[3];
       const int64_t Yo = out.shape[2], Xo = out.shape[3], K = C * U * V, YX = Yo * Xo;
       int64_t ld = 0;
-      float* col = im2col(a, U, V, Yo, Xo, true, ld);
+      const int64_t img = pitch4(YX);
+      float* col = im2col(a, U, V, Yo, Xo, img, ld);
       const MatView km = filter(b);
       for (int64_t i = 0; i < NB; ++i) {
         GemmSpec s;
         s.a = km;
-        s.b = MatView{col + i * YX * ld, YX, K, ld, 1};
-        s.tb = true;
+        s.b = MatView{col + i * img, K, YX, ld, 1};  // [K x YX] row-major (MN-major operand)
         s.c = out.ptr + i * O * YX;
         s.c_rs = YX;
         specs.push_back(s);
       }
       flops = 2.0 * double(NB) * double(O) * double(YX) * double(K);
     } else if (op.mode == ConvMode::grad_weight) {
+      // gk[o, cuv] = Gp[o, (n,yx)] . col[cuv, (n,yx)]^T
       const int64_t NB = a.shape[0], C = a.shape[1], O = b.shape[1], Yo = b.shape[2], Xo = b.shape[3];
       const int64_t U = out.shape[2], V = out.shape[3], K = C * U * V, YX = Yo * Xo;
       int64_t ld = 0;
-      float* col = im2col(a, U, V, Yo, Xo, false, ld);  // [cuv][(n, yx)]
-      // G[n, o, y, x] -> Gp[o][(n, y, x)] (rows padded to 16 bytes)
+      const int64_t img = pitch4(YX);
+      float* col = im2col(a, U, V, Yo, Xo, img, ld);  // shared with the layer's forward
+      // G[n, o, y, x] -> Gp[o][(n, img-strided y, x)] (padding columns stay 0: zeroed arena)
       if (!o_pre.descs.empty() && o_pre_op != op.id) flush();
       o_pre_op = op.id;
       float* gp = alloc_bytes(size_t(O * ld) * 4);
@@ -383,17 +399,19 @@ struct Lowerer {
       src.st[0] = b.st[1]; src.st[1] = b.st[0];
       dst.ptr = gp;
       dst.shape[0] = O; dst.shape[1] = NB;
-      dst.st[0] = ld; dst.st[1] = YX; dst.st[2] = Xo; dst.st[3] = 1;
+      dst.st[0] = ld; dst.st[1] = img; dst.st[2] = Xo; dst.st[3] = 1;
       o_pre.descs.push_back(nary_desc(NARY_COPY, dst, {src}));
-      GemmSpec s;
-      s.a = MatView{gp, O, NB * YX, ld, 1};
-      s.b = MatView{col, K, NB * YX, ld, 1};
+      GemmSpec s;  // contraction over all images' (padded) columns; pads are 0 in both operands
+      s.a = MatView{gp, O, NB * img, ld, 1};
+      s.b = MatView{col, K, NB * img, ld, 1};
       s.tb = true;
       s.c = out.ptr;
       s.c_rs = K;
       specs.push_back(s);
       flops = 2.0 * double(O) * double(K) * double(NB * YX);
     } else {
+      // dcol[cuv, n*YX + yx] = Kmat[o, cuv]^T . G_n[o, yx]   (one problem per image), then
+      // col2im: h[n,c,y,x] = sum_{u,v} dcol[(c,u,v), n*YX + (y-u)*Xo + (x-v)]
       const int64_t NB = a.shape[0], O = a.shape[1], Yo = a.shape[2], Xo = a.shape[3];
       const int64_t C = b.shape[1], U = b.shape[2], V = b.shape[3], K = C * U * V, YX = Yo * Xo;
       const MatView km = filter(b);
@@ -401,14 +419,14 @@ struct Lowerer {
       if (!(g.st[3] == 1 && g.st[2] == Xo && g.st[1] % 4 == 0 && g.st[0] % 4 == 0 &&
             (reinterpret_cast<uintptr_t>(g.ptr) & 15) == 0))
         g = padded_copy(a, 2, op.id);
-      const int64_t ld = pitch4(K);
-      float* dcol = alloc_bytes(size_t(NB * YX * ld) * 4);
+      const int64_t img = pitch4(YX), ld = pitch4(NB * img);
+      float* dcol = alloc_bytes(size_t(K * ld) * 4);
       for (int64_t i = 0; i < NB; ++i) {
         GemmSpec s;
-        s.a = MatView{g.ptr + i * g.st[0], O, YX, g.st[1], 1};  // G_n [o, yx], used transposed
+        s.a = km;                                                // Kmat [o, cuv], used transposed
         s.ta = true;
-        s.b = km;                                                // Kmat [o, cuv]
-        s.c = dcol + i * YX * ld;
+        s.b = MatView{g.ptr + i * g.st[0], O, YX, g.st[1], 1};  // G_n [o, yx] (K x N)
+        s.c = dcol + i * img;
         s.c_rs = ld;
         specs.push_back(s);
       }
@@ -416,9 +434,10 @@ struct Lowerer {
       std::memset(&d, 0, sizeof d);
       d.mode = CONV_COL2IM;
       d.a.ptr = dcol;
+      d.a.shape[0] = NB;
       d.out = out.ptr;
-      d.n = out.elements();
-      d.p[0] = C; d.p[1] = U; d.p[2] = V; d.p[3] = Yo; d.p[4] = Xo; d.p[5] = ld;
+      d.n = out.elements() / out.shape[3];  // rows (n, c, y)
+      d.p[0] = C; d.p[1] = U; d.p[2] = V; d.p[3] = Yo; d.p[4] = Xo; d.p[5] = ld; d.p[6] = img;
       o_post.descs.push_back(d);
       flops = 2.0 * double(NB) * double(YX) * double(K) * double(O);
     }
@@ -869,6 +888,9 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
     }
     P->arena_bytes = std::max<size_t>(P->arena_used, kAlign);
     CUDA_CHECK(cudaMalloc(&P->arena, P->arena_bytes));
+    // scratch padding (16-byte rows of im2col matrices, per-image column blocks) is read as
+    // zero by the GEMMs and never written
+    CUDA_CHECK(cudaMemset(P->arena, 0, P->arena_bytes));
     P->base = reinterpret_cast<uintptr_t>(P->arena);
     lower(*P, false);
     prepare_program(*P, P->main);

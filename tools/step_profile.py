@@ -1,0 +1,37 @@
+"""Per lowered step device times (CUDA events) of one plan: where a train step's time goes.
+
+    python tools/step_profile.py <plan stem under plans/> [top]"""
+import gzip
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1805_04170_b200.executor import FLAG_FUSE, Context, PlanExecutor  # noqa: E402
+
+stem = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+text = gzip.open(os.path.join(ROOT, "plans", stem + ".plan.json.gz"), "rt").read()
+ex = PlanExecutor(Context(0), text, precision=0, flags=FLAG_FUSE)
+ex.init_inputs(7)
+for _ in range(3):
+    ex.execute()
+ex.enable_timing(True)
+runs = []
+for _ in range(5):
+    ex.execute()
+    runs.append(ex.last_step_times())
+ms = [statistics.median(x) for x in zip(*runs)]
+steps = ex.describe()["main"]["steps"]
+tot = sum(ms)
+print(f"{stem}: {len(steps)} steps, {tot:.3f} ms")
+by = {}
+for st, t in zip(steps, ms):
+    key = (st["kind"], st["what"])
+    by[key] = by.get(key, 0.0) + t
+for key, t in sorted(by.items(), key=lambda kv: -kv[1]):
+    print(f"  {key[0]:5s} {key[1]:12s} {t:8.3f} ms {100 * t / tot:5.1f}%")
+for st, t in sorted(zip(steps, ms), key=lambda p: -p[1])[:top]:
+    extra = st.get("shapes", [[]])[0] if st["kind"] == "gemm" else st.get("descs", st.get("bytes", ""))
+    print(f"  {t:8.3f} ms  {st['kind']:5s} {st['what']:12s} {st['op']:10s} {extra}")
