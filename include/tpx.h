@@ -125,9 +125,11 @@ int tpx_last_step_times(const tpx_plan* plan, double* ms, int64_t n, int64_t* n_
 int tpx_enable_timing(tpx_plan* plan, int on);
 
 /* ---------------------------------------------------------------- kernel-level entry points
- * Device pointers (fp32).  Used by the kernel tests; the plan executor calls the same code.
- * out = op(A) . op(B) (run_matmul, dense.cpp:71-90); a/b are row-major views with row
- * strides (elements).  epi_* optionally chain elementwise stages onto the product. */
+ * Device pointers, fp32 storage (precision 0 = TF32, 1 = 3xTF32 fp32-accurate) or bf16 storage
+ * (precision 2: every operand, output and epilogue operand is bf16; fp32 accumulate).  Used by
+ * the kernel tests; the plan executor calls the same code.  out = op(A) . op(B) (run_matmul,
+ * dense.cpp:71-90); a/b are row-major views with row strides (elements).  epi_* optionally
+ * chain elementwise stages onto the product. */
 int tpx_gemm(const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs, const float* b,
              int64_t b_rows, int64_t b_cols, int64_t b_rs, int transpose_a, int transpose_b,
              float* c, int64_t c_rs, int n_epi, const int* epi_ops, const float* epi_scales,

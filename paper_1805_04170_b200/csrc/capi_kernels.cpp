@@ -30,7 +30,9 @@ __attribute__((visibility("default"))) int tpx_gemm_timed(
     uint64_t cuda_stream, int warmup, int iters, double* avg_ms) {
   return tpx::guard([&] {
     if (n_epi < 0 || n_epi > tpx::kMaxEpi) tpx::fail("tpx_gemm: too many epilogue stages");
+    if (precision < 0 || precision > 2) tpx::fail("tpx_gemm: precision must be 0 (tf32), 1 (3xtf32) or 2 (bf16)");
     tpx::GemmSpec s;
+    s.bf16 = precision == 2;
     s.a = {a, a_rows, a_cols, a_rs, 1};
     s.b = {b, b_rows, b_cols, b_rs, 1};
     s.ta = transpose_a != 0;
@@ -52,7 +54,7 @@ __attribute__((visibility("default"))) int tpx_gemm_timed(
     int dev = 0, sms = 148;
     CUDA_CHECK(cudaGetDevice(&dev));
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    tpx::GemmLaunch g = tpx::gemm_prepare({s}, sms, precision == 1);
+    tpx::GemmLaunch g = tpx::gemm_prepare({s}, sms, precision == 1);  // 2: bf16 storage (GemmSpec.bf16)
     cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     try {

@@ -27,6 +27,8 @@
 #include <cstring>
 #include <stdexcept>
 
+#include <cuda_bf16.h>
+
 #include "ptx.cuh"
 #include "util.h"
 
@@ -109,23 +111,76 @@ __device__ __forceinline__ void epi_apply(int op, float (&v)[CW], const float (&
 
 __device__ __forceinline__ bool epi_needs_other(int op) { return op >= EPI_ADD; }
 
+// ---- storage-type access (B = bf16 storage, else fp32).  Global pointers are opaque `float*`
+// addresses with element offsets; 4-element vector accesses are 16 B (fp32) or 8 B (bf16).
+template <bool B>
+__device__ __forceinline__ float ld1(const float* base, long long i) {
+  if constexpr (B) return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(base) + i));
+  else return __ldg(base + i);
+}
+template <bool B>
+__device__ __forceinline__ void st1(float* base, long long i, float v) {
+  if constexpr (B) reinterpret_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(v);
+  else base[i] = v;
+}
+template <bool B>
+__device__ __forceinline__ float4 ld4(const float* base, long long i) {
+  if constexpr (B) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(base) + i));
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  } else {
+    return __ldg(reinterpret_cast<const float4*>(base + i));
+  }
+}
+template <bool B>
+__device__ __forceinline__ void st4(float* base, long long i, float4 v, bool stream) {
+  if constexpr (B) {
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&a);
+    u.y = *reinterpret_cast<const uint32_t*>(&b);
+    uint2* d = reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(base) + i);
+    if (stream) __stcs(d, u);
+    else *d = u;
+  } else {
+    float4* d = reinterpret_cast<float4*>(base + i);
+    if (stream) __stcs(d, v);
+    else *d = v;
+  }
+}
+// value as stored (fused stages consume the rounded value, exactly like the unfused launch)
+template <bool B>
+__device__ __forceinline__ float rnd(float v) {
+  if constexpr (B) return __bfloat162float(__float2bfloat16_rn(v));
+  else return v;
+}
+// base + i elements is 4-element (vector) aligned
+template <bool B>
+__device__ __forceinline__ bool vec_aligned(const float* base, long long i) {
+  return ((reinterpret_cast<uintptr_t>(base) + uintptr_t(i) * (B ? 2 : 4)) & (B ? 7 : 15)) == 0;
+}
+
 // Store CW consecutive columns [q0, q0+CW) of row p.  Used for swapped problems (rs == 1):
-// the warp's 32 rows are 32 consecutive floats, so every scalar store is one 128-byte line.
+// the warp's 32 rows are 32 consecutive elements, so every scalar store is one line.
+template <bool B>
 __device__ __forceinline__ void store_chunk(float* base, long long rs, long long cs, int p,
                                             int q0, int P, int Q, const float (&v)[CW]) {
   if (p >= P) return;
-  float* row = base + (long long)p * rs;
-  if (cs == 1 && q0 + CW <= Q && ((reinterpret_cast<uintptr_t>(row + q0) & 15) == 0)) {
-    float4* d = reinterpret_cast<float4*>(row + q0);
+  const long long row = (long long)p * rs;
+  if (cs == 1 && q0 + CW <= Q && vec_aligned<B>(base, row + q0)) {
 #pragma unroll
-    for (int j = 0; j < CW / 4; ++j) d[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    for (int j = 0; j < CW / 4; ++j)
+      st4<B>(base, row + q0 + 4 * j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]), false);
   } else {
 #pragma unroll
     for (int j = 0; j < CW; ++j)
-      if (q0 + j < Q) row[(long long)(q0 + j) * cs] = v[j];
+      if (q0 + j < Q) st1<B>(base, row + (long long)(q0 + j) * cs, v[j]);
   }
 }
 
+template <bool B>
 __device__ __forceinline__ void load_chunk(const float* base, long long rs, long long cs, int p,
                                            int q0, int P, int Q, float (&v)[CW]) {
   if (p >= P) {
@@ -133,17 +188,16 @@ __device__ __forceinline__ void load_chunk(const float* base, long long rs, long
     for (int j = 0; j < CW; ++j) v[j] = 0.f;
     return;
   }
-  const float* row = base + (long long)p * rs;
-  if (cs == 1 && q0 + CW <= Q && ((reinterpret_cast<uintptr_t>(row + q0) & 15) == 0)) {
-    const float4* s = reinterpret_cast<const float4*>(row + q0);
+  const long long row = (long long)p * rs;
+  if (cs == 1 && q0 + CW <= Q && vec_aligned<B>(base, row + q0)) {
 #pragma unroll
     for (int j = 0; j < CW / 4; ++j) {
-      float4 t = __ldg(s + j);
+      const float4 t = ld4<B>(base, row + q0 + 4 * j);
       v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < CW; ++j) v[j] = (q0 + j < Q) ? __ldg(row + (long long)(q0 + j) * cs) : 0.f;
+    for (int j = 0; j < CW; ++j) v[j] = (q0 + j < Q) ? ld1<B>(base, row + (long long)(q0 + j) * cs) : 0.f;
   }
 }
 
@@ -160,9 +214,34 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
   return r;
 }
 
+// Elementwise-operand box (TMA): fp32 boxes are 32 x CW with the 64-byte swizzle (box_off);
+// bf16 boxes are 32 x CW unswizzled (32-byte rows).  Store order: row r, columns 4c..4c+3.
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 r;
+  asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(a) : "memory");
+  return r;
+}
+__device__ __forceinline__ float4 bf16x4(uint2 u) {
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+template <bool B>
+__device__ __forceinline__ float4 obox_so(uint32_t ob, int r, int c) {
+  if constexpr (B) return bf16x4(lds64(ob + r * (CW * 2) + c * 8));
+  else return lds128(ob + box_off(r, c));
+}
+// row `r`, 4 columns starting at 4j (row-order epilogue)
+template <bool B>
+__device__ __forceinline__ float4 obox_row(uint32_t ob, int r, int j) {
+  if constexpr (B) return bf16x4(lds64(ob + r * (CW * 2) + j * 8));
+  else return lds128(ob + box_off(r, j));
+}
+
 // Store a warp's 32 x CW block (thread = row `lane`, CW consecutive columns) into a row-major
 // global view, transposed through a swizzled smem box so that each warp store instruction
-// writes 8 rows x 64 contiguous bytes.  Rows >= P and columns >= Q are masked.
+// writes 8 rows x CW contiguous elements.  Rows >= P and columns >= Q are masked.
+template <bool B>
 __device__ __forceinline__ void store_block(uint32_t sbuf, int lane, const float (&v)[CW], float* base,
                                             long long rs, int prow0, int q0, int P, int Q, bool stream) {
 #pragma unroll
@@ -170,22 +249,21 @@ __device__ __forceinline__ void store_block(uint32_t sbuf, int lane, const float
   __syncwarp();
   const int c = lane & 3;
   const int gq = q0 + c * 4;
-  const bool vec = ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && ((rs & 3) == 0);
+  const bool vec = vec_aligned<B>(base, 0) && ((rs & 3) == 0);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = i * 8 + (lane >> 2);
     const float4 x = lds128(sbuf + box_off(r, c));
     const int gp = prow0 + r;
     if (gp < P) {
-      float* dst = base + (long long)gp * rs + gq;
+      const long long o = (long long)gp * rs + gq;
       if (vec && gq + 4 <= Q) {
-        if (stream) __stcs(reinterpret_cast<float4*>(dst), x);  // evict-first: not re-read soon
-        else *reinterpret_cast<float4*>(dst) = x;
+        st4<B>(base, o, x, stream);
       } else {
-        if (gq < Q) dst[0] = x.x;
-        if (gq + 1 < Q) dst[1] = x.y;
-        if (gq + 2 < Q) dst[2] = x.z;
-        if (gq + 3 < Q) dst[3] = x.w;
+        if (gq < Q) st1<B>(base, o, x.x);
+        if (gq + 1 < Q) st1<B>(base, o + 1, x.y);
+        if (gq + 2 < Q) st1<B>(base, o + 2, x.z);
+        if (gq + 3 < Q) st1<B>(base, o + 3, x.w);
       }
     }
   }
@@ -214,26 +292,33 @@ __device__ __forceinline__ void epi_apply4(int op, float4 (&x)[4], const float4 
   }
 }
 // Store-order block store: x[i] = row (i*8 + lane/4), columns q0 + 4*(lane%4) .. +3 of a warp's
-// 32 x CW block; each instruction writes 8 rows x 64 contiguous bytes.
+// 32 x CW block; each instruction writes 8 rows x CW contiguous elements.
+template <bool B>
 __device__ __forceinline__ void store_block_so(const float4 (&x)[4], int lane, float* base, long long rs,
                                                int prow0, int q0, int P, int Q, bool stream) {
   const int gq = q0 + (lane & 3) * 4;
-  const bool vec = ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && ((rs & 3) == 0);
+  const bool vec = vec_aligned<B>(base, 0) && ((rs & 3) == 0);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int gp = prow0 + i * 8 + (lane >> 2);
     if (gp < P) {
-      float* dst = base + (long long)gp * rs + gq;
+      const long long o = (long long)gp * rs + gq;
       if (vec && gq + 4 <= Q) {
-        if (stream) __stcs(reinterpret_cast<float4*>(dst), x[i]);
-        else *reinterpret_cast<float4*>(dst) = x[i];
+        st4<B>(base, o, x[i], stream);
       } else {
-        if (gq < Q) dst[0] = x[i].x;
-        if (gq + 1 < Q) dst[1] = x[i].y;
-        if (gq + 2 < Q) dst[2] = x[i].z;
-        if (gq + 3 < Q) dst[3] = x[i].w;
+        if (gq < Q) st1<B>(base, o, x[i].x);
+        if (gq + 1 < Q) st1<B>(base, o + 1, x[i].y);
+        if (gq + 2 < Q) st1<B>(base, o + 2, x[i].z);
+        if (gq + 3 < Q) st1<B>(base, o + 3, x[i].w);
       }
     }
+  }
+}
+template <bool B>
+__device__ __forceinline__ void round4(float4 (&x)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[i].x = rnd<B>(x[i].x); x[i].y = rnd<B>(x[i].y); x[i].z = rnd<B>(x[i].z); x[i].w = rnd<B>(x[i].w);
   }
 }
 
@@ -259,13 +344,21 @@ __device__ __forceinline__ float4* ws_ptr(float* ws, int slot, int bn, int c0, i
 // PAIR = CTA pair (cluster of 2, tcgen05 cta_group::2): one 256 x BN tile per pair; each CTA
 // stages its 128 rows of A and BN/2 columns of B (half the operand bytes per CTA), the leader
 // issues the M = 256 MMAs, and each CTA drains its own 128 accumulator rows.
-template <int BN, bool P_MN, bool Q_MN, bool SPLIT, bool PAIR>
+// BF16 = bf16 storage: kind::f16 MMAs on bf16 operands (64-element k-blocks), fp32
+// accumulators, epilogue stages computed in fp32 and stored rounded to bf16.
+template <int BN, bool P_MN, bool Q_MN, bool SPLIT, bool PAIR, bool BF16>
 __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     gemm_tf32_kernel(const GemmProblem* __restrict__ probs, const GemmSeg* __restrict__ segs,
                      const int* __restrict__ seg_off, float* __restrict__ ws,
                      unsigned* __restrict__ flags, const int STAGES, const int PF,
                      const int has_other) {
   static_assert(!(PAIR && SPLIT), "3xTF32 runs on single-CTA tiles");
+  static_assert(!(BF16 && SPLIT), "3xTF32 is an fp32-storage mode");
+  constexpr int ES = BF16 ? 2 : 4;                  // storage bytes per element
+  constexpr int BKE = 128 / ES;                     // k per k-block (one 128-byte smem row)
+  constexpr int MNC = 128 / ES;                     // MN elements per MN-major chunk
+  constexpr uint32_t MNCH = uint32_t(BKE) * 128u;   // bytes of one MN-major chunk (BKE k-rows)
+  constexpr int KPM = BF16 ? 16 : 8;                // k per MMA instruction (32 bytes)
   constexpr int BNH = PAIR ? BN / 2 : BN;     // B columns staged by this CTA
   constexpr int PBM = PAIR ? 2 * BM : BM;     // rows of one (pair) tile
   constexpr uint32_t A_BYTES = BM * BK * 4;
@@ -273,8 +366,9 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   constexpr uint32_t STAGE = stage_bytes(BNH, SPLIT);
   constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
   constexpr int NEPI = epi_warps(SPLIT);
+  constexpr uint32_t FMT = BF16 ? 1u : 2u;          // A/B format: bf16 (kind::f16) / tf32
   constexpr uint32_t IDESC = (1u << 4)                 // D format f32
-                             | (2u << 7) | (2u << 10)  // A, B format tf32
+                             | (FMT << 7) | (FMT << 10)
                              | (uint32_t(P_MN) << 15) | (uint32_t(Q_MN) << 16) |
                              (uint32_t(BN >> 3) << 17) | (uint32_t(PBM >> 4) << 24);
 
@@ -335,22 +429,22 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   // bar: local barrier (single CTA); bar_c: the leader's barrier in the cluster window (pair)
   auto load_kblock = [&](const GemmProblem& pr, int kb, int p0, int q0, uint8_t* sa, uint8_t* sb,
                          uint64_t* bar, uint32_t bar_c, uint64_t pol_a, uint64_t pol_b) {
-    const int k0 = kb * BK;
+    const int k0 = kb * BKE;
     if constexpr (!P_MN) {
       ld2(sa, pr.tmap_a, bar, bar_c, k0, p0, pol_a);
     } else if (pr.a3d) {
-      ld3(sa, pr.tmap_a, bar, bar_c, 0, k0, p0 / 32, pol_a);
+      ld3(sa, pr.tmap_a, bar, bar_c, 0, k0, p0 / MNC, pol_a);
     } else {
 #pragma unroll
-      for (int j = 0; j < BM / 32; ++j) ld2(sa + j * 4096, pr.tmap_a, bar, bar_c, p0 + 32 * j, k0, pol_a);
+      for (int j = 0; j < BM / MNC; ++j) ld2(sa + j * MNCH, pr.tmap_a, bar, bar_c, p0 + MNC * j, k0, pol_a);
     }
     if constexpr (!Q_MN) {
       ld2(sb, pr.tmap_b, bar, bar_c, k0, q0, pol_b);
     } else if (pr.b3d) {
-      ld3(sb, pr.tmap_b, bar, bar_c, 0, k0, q0 / 32, pol_b);
+      ld3(sb, pr.tmap_b, bar, bar_c, 0, k0, q0 / MNC, pol_b);
     } else {
 #pragma unroll
-      for (int j = 0; j < BNH / 32; ++j) ld2(sb + j * 4096, pr.tmap_b, bar, bar_c, q0 + 32 * j, k0, pol_b);
+      for (int j = 0; j < BNH / MNC; ++j) ld2(sb + j * MNCH, pr.tmap_b, bar, bar_c, q0 + MNC * j, k0, pol_b);
     }
   };
   if (warp == 0 && lane == 0) {
@@ -387,14 +481,18 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         const uint32_t sa = smem_u32(smem + s * STAGE);
         const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
+        for (int kk = 0; kk < BKE / KPM; ++kk) {
           // K-major: 128B rows of K, 8-row atoms (SBO 1024), K step = +32 bytes.
-          // MN-major: 128B rows of M/N per k, 32-byte-granule swizzle, 4-row groups (SBO 512),
-          //           32-column chunks 4096 bytes apart (LBO), K step = 8 rows = +1024 bytes.
-          const uint64_t ad = P_MN ? umma_desc(sa + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1)
-                                   : umma_desc(sa + kk * 32, 16, 1024, 2);
-          const uint64_t bd = Q_MN ? umma_desc(sb + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1)
-                                   : umma_desc(sb + kk * 32, 16, 1024, 2);
+          // MN-major tf32: 128B rows of M/N per k, 32-byte-granule swizzle, 4-row groups
+          //   (SBO 512), 32-column chunks 4096 bytes apart (LBO), K step = 8 rows = +1024 bytes.
+          // MN-major bf16: 128-byte swizzle, 8-row atoms (SBO 1024), 64-column chunks 8192 bytes
+          //   apart (LBO), K step = 16 rows = +2048 bytes.
+          const uint64_t ad = !P_MN ? umma_desc(sa + kk * 32, 16, 1024, 2)
+                              : BF16 ? umma_desc(sa + kk * 2048, MNCH, 1024, 2)
+                                     : umma_desc(sa + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1);
+          const uint64_t bd = !Q_MN ? umma_desc(sb + kk * 32, 16, 1024, 2)
+                              : BF16 ? umma_desc(sb + kk * 2048, MNCH, 1024, 2)
+                                     : umma_desc(sb + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1);
           const uint32_t accum = (kb > sg.kb0 || kk > 0) ? 1u : 0u;
           if constexpr (SPLIT) {
             // low parts live OPB bytes after the high parts, in the same (swizzled) layout
@@ -403,9 +501,11 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             mma_tf32(d, ad, bd + lo, IDESC, 1u);
             mma_tf32(d, ad, bd, IDESC, 1u);
           } else if constexpr (PAIR) {
-            mma_tf32_pair(d, ad, bd, IDESC, accum);
+            if constexpr (BF16) mma_f16_pair(d, ad, bd, IDESC, accum);
+            else mma_tf32_pair(d, ad, bd, IDESC, accum);
           } else {
-            mma_tf32(d, ad, bd, IDESC, accum);
+            if constexpr (BF16) mma_f16(d, ad, bd, IDESC, accum);
+            else mma_tf32(d, ad, bd, IDESC, accum);
           }
         }
         if constexpr (PAIR) mma_commit_pair(&empty[s], 0x3);  // frees the slot in both CTAs
@@ -472,7 +572,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         if (imap && ic0 < c_end && iq + ic0 < iQ) {
           uint64_t* bar = &other_bar[ew * ODEPTH + i_slot];
           fence_proxy_async_smem();
-          mbar_arrive_expect_tx(bar, kOutStage);
+          mbar_arrive_expect_tx(bar, uint32_t(32 * CW * ES));  // one 32 x CW operand box
           tma_load_2d_hint(other_stage + (ew * ODEPTH + i_slot) * kOutStage, imap, bar, iq + ic0, ip, o_policy);
           if (++i_slot == uint32_t(ODEPTH)) i_slot = 0;
           ic0 += CSTEP;
@@ -573,16 +673,16 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         // patterns the lowering emits (act, dact, act+seed, step+upd) so the hot loop is
         // straight-line code.
         const int c = lane & 3;
-        float* dp[1 + kMaxEpi];
+        long long dofs[1 + kMaxEpi];  // element offset of (row prow0 + lane/4, column 4c)
         long long st8[1 + kMaxEpi];
         bool vec_ok = true;
 #pragma unroll
         for (int e = 0; e <= kMaxEpi; ++e) {
-          dp[e] = nullptr;
+          dofs[e] = 0;
           st8[e] = 0;
           if (e < nout) {
-            vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(obase[e]) & 15) == 0) && ((ors[e] & 3) == 0);
-            dp[e] = obase[e] + (long long)(prow0 + (lane >> 2)) * ors[e] + c * 4;
+            vec_ok = vec_ok && vec_aligned<BF16>(obase[e], 0) && ((ors[e] & 3) == 0);
+            dofs[e] = (long long)(prow0 + (lane >> 2)) * ors[e] + c * 4;
             st8[e] = 8ll * ors[e];
           }
         }
@@ -631,38 +731,36 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             mbar_wait(&other_bar[ew * ODEPTH + o_slot], o_phase);
             const uint32_t ob = smem_u32(other_stage + (ew * ODEPTH + o_slot) * kOutStage);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) ox[i] = lds128(ob + box_off(i * 8 + (lane >> 2), c));
+            for (int i = 0; i < 4; ++i) ox[i] = obox_so<BF16>(ob, i * 8 + (lane >> 2), c);
             if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
           }
           __syncwarp();  // transpose box and operand box free again
           if (oe >= 0 && lane == 0) issue_other();
           const bool full_blk = vec_ok && rows_in && q0 + CW <= QQ;
           const int gq = q0 + c * 4;
+          // store stage e's values, then round them as stored (the next stage reads the stored
+          // value, like the unfused launch would)
           auto put = [&](int e) {
-            float* d0 = dp[e] + q0;
+            const long long d0 = dofs[e] + q0;
             if (full_blk) {
-              if (ostream) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) __stcs(reinterpret_cast<float4*>(d0 + i * st8[e]), x[i]);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) *reinterpret_cast<float4*>(d0 + i * st8[e]) = x[i];
-              }
+              for (int i = 0; i < 4; ++i) st4<BF16>(obase[e], d0 + i * st8[e], x[i], ostream);
             } else {
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 if (prow0 + i * 8 + (lane >> 2) >= PP) continue;
-                float* d = d0 + i * st8[e];
+                const long long d = d0 + i * st8[e];
                 if (vec_ok && gq + 4 <= QQ) {
-                  *reinterpret_cast<float4*>(d) = x[i];
+                  st4<BF16>(obase[e], d, x[i], false);
                 } else {
-                  if (gq < QQ) d[0] = x[i].x;
-                  if (gq + 1 < QQ) d[1] = x[i].y;
-                  if (gq + 2 < QQ) d[2] = x[i].z;
-                  if (gq + 3 < QQ) d[3] = x[i].w;
+                  if (gq < QQ) st1<BF16>(obase[e], d, x[i].x);
+                  if (gq + 1 < QQ) st1<BF16>(obase[e], d + 1, x[i].y);
+                  if (gq + 2 < QQ) st1<BF16>(obase[e], d + 2, x[i].z);
+                  if (gq + 3 < QQ) st1<BF16>(obase[e], d + 3, x[i].w);
                 }
               }
             }
+            round4<BF16>(x);
           };
           switch (chain) {
             case 0:
@@ -719,14 +817,14 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             const uint32_t ob = smem_u32(other_stage + (ew * ODEPTH + o_slot) * kOutStage);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
-              const float4 x = lds128(ob + box_off(lane, j));
+              const float4 x = obox_row<BF16>(ob, lane, j);
               o[4 * j] = x.x; o[4 * j + 1] = x.y; o[4 * j + 2] = x.z; o[4 * j + 3] = x.w;
             }
             if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
             __syncwarp();
             if (lane == 0) issue_other();
           } else {
-            load_chunk(pr.epi[oe].other, pr.epi[oe].o_rs, pr.epi[oe].o_cs, p, q0, PP, QQ, o);
+            load_chunk<BF16>(pr.epi[oe].other, pr.epi[oe].o_rs, pr.epi[oe].o_cs, p, q0, PP, QQ, o);
           }
         }
         float v[CW];
@@ -758,12 +856,14 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
           if (e > 0) {
             if (epi_needs_other(eop[e - 1]) && e - 1 != oe) {
               const EpiStage& st = pr.epi[e - 1];
-              load_chunk(st.other, st.o_rs, st.o_cs, p, q0, PP, QQ, o);
+              load_chunk<BF16>(st.other, st.o_rs, st.o_cs, p, q0, PP, QQ, o);
             }
             epi_apply(eop[e - 1], v, o, esc[e - 1]);
           }
-          if (ocs[e] == 1) store_block(sbuf, lane, v, obase[e], ors[e], prow0, q0, PP, QQ, ostream);
-          else store_chunk(obase[e], ors[e], ocs[e], p, q0, PP, QQ, v);  // swapped: lanes consecutive
+          if (ocs[e] == 1) store_block<BF16>(sbuf, lane, v, obase[e], ors[e], prow0, q0, PP, QQ, ostream);
+          else store_chunk<BF16>(obase[e], ors[e], ocs[e], p, q0, PP, QQ, v);  // swapped: lanes consecutive
+#pragma unroll
+          for (int j = 0; j < CW; ++j) v[j] = rnd<BF16>(v[j]);  // the next stage reads the stored value
         }
       }
     }
@@ -780,26 +880,33 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
 
 using KernelFn = void (*)(const GemmProblem*, const GemmSeg*, const int*, float*, unsigned*, int, int, int);
 
-template <int BN, bool SPLIT, bool PAIR>
+template <int BN, bool SPLIT, bool PAIR, bool BF16>
 KernelFn pick(bool p_mn, bool q_mn) {
-  if (!p_mn && !q_mn) return gemm_tf32_kernel<BN, false, false, SPLIT, PAIR>;
-  if (!p_mn && q_mn) return gemm_tf32_kernel<BN, false, true, SPLIT, PAIR>;
-  if (p_mn && !q_mn) return gemm_tf32_kernel<BN, true, false, SPLIT, PAIR>;
-  return gemm_tf32_kernel<BN, true, true, SPLIT, PAIR>;
+  if (!p_mn && !q_mn) return gemm_tf32_kernel<BN, false, false, SPLIT, PAIR, BF16>;
+  if (!p_mn && q_mn) return gemm_tf32_kernel<BN, false, true, SPLIT, PAIR, BF16>;
+  if (p_mn && !q_mn) return gemm_tf32_kernel<BN, true, false, SPLIT, PAIR, BF16>;
+  return gemm_tf32_kernel<BN, true, true, SPLIT, PAIR, BF16>;
 }
 
-KernelFn kernel_for(int bn, bool p_mn, bool q_mn, bool split, bool pair) {
+template <bool BF16>
+KernelFn kernel_for_t(int bn, bool p_mn, bool q_mn, bool split, bool pair) {
   if (pair) {
-    if (bn != 256 || split) throw std::runtime_error("gemm: CTA-pair tiles are 256 x 256 TF32 only");
-    return pick<256, false, true>(p_mn, q_mn);
+    if (bn != 256 || split) throw std::runtime_error("gemm: CTA-pair tiles are 256 x 256 single-pass only");
+    return pick<256, false, true, BF16>(p_mn, q_mn);
   }
+  if (BF16 && split) throw std::runtime_error("gemm: 3xTF32 is an fp32-storage mode");
+  constexpr bool S = !BF16;  // the split variants exist for fp32 storage only
   switch (bn) {
-    case 32: return split ? pick<32, true, false>(p_mn, q_mn) : pick<32, false, false>(p_mn, q_mn);
-    case 64: return split ? pick<64, true, false>(p_mn, q_mn) : pick<64, false, false>(p_mn, q_mn);
-    case 128: return split ? pick<128, true, false>(p_mn, q_mn) : pick<128, false, false>(p_mn, q_mn);
-    case 256: return split ? pick<256, true, false>(p_mn, q_mn) : pick<256, false, false>(p_mn, q_mn);
+    case 32: return split ? pick<32, S, false, BF16>(p_mn, q_mn) : pick<32, false, false, BF16>(p_mn, q_mn);
+    case 64: return split ? pick<64, S, false, BF16>(p_mn, q_mn) : pick<64, false, false, BF16>(p_mn, q_mn);
+    case 128: return split ? pick<128, S, false, BF16>(p_mn, q_mn) : pick<128, false, false, BF16>(p_mn, q_mn);
+    case 256: return split ? pick<256, S, false, BF16>(p_mn, q_mn) : pick<256, false, false, BF16>(p_mn, q_mn);
   }
   throw std::runtime_error("gemm: unsupported tile width " + std::to_string(bn));
+}
+
+KernelFn kernel_for(int bn, bool p_mn, bool q_mn, bool split, bool pair, bool bf16) {
+  return bf16 ? kernel_for_t<true>(bn, p_mn, q_mn, split, pair) : kernel_for_t<false>(bn, p_mn, q_mn, split, pair);
 }
 
 unsigned g_dbg_lbo = 0, g_dbg_sbo = 0;
@@ -832,20 +939,27 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D fp32 tensor map over a row-major view: `inner` contiguous elements per row, `outer`
-// rows `row_stride` elements apart, boxes of box_inner x box_outer, 128-byte swizzle.
+// 2-D tensor map over a row-major view: `inner` contiguous elements per row, `outer` rows
+// `row_stride` elements apart, boxes of box_inner x box_outer.  fp32: 128-byte swizzle (32-byte
+// atoms for MN-major tf32 operands); bf16: 128-byte swizzle.  `sw64` = the epilogue operand box
+// (fp32: 64-byte swizzle; bf16: 32-byte rows, unswizzled).
 void make_map(CUtensorMap* m, const float* base, long long inner, long long outer,
-              long long row_stride, int box_inner, int box_outer, bool mn_major, bool sw64 = false) {
+              long long row_stride, int box_inner, int box_outer, bool mn_major, bool sw64 = false,
+              bool bf16 = false) {
+  const int es = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   // a single row's stride is never used, but the encoder wants it 16-byte aligned
-  const long long rs = outer > 1 ? std::max<long long>(row_stride, inner) : (inner + 3) / 4 * 4;
-  cuuint64_t strides[1] = {(cuuint64_t)(rs * 4)};
+  const long long al = 16 / es;
+  const long long rs = outer > 1 ? std::max<long long>(row_stride, inner) : (inner + al - 1) / al * al;
+  cuuint64_t strides[1] = {(cuuint64_t)(rs * es)};
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           sw64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                : mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+  const CUtensorMapSwizzle sw = sw64 ? (bf16 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B)
+                                : (mn_major && !bf16) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                                      : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = encode_fn()(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                           const_cast<float*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           sw,
                            // 64-byte operand rows: no promotion (a promoted 256 B line would be
                            // evicted, evict-first, before the next chunks use it)
                            sw64 ? kOtherPromo[g_other_promo & 3] : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -854,18 +968,21 @@ void make_map(CUtensorMap* m, const float* base, long long inner, long long oute
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
-// 3-D map of an MN-major operand whose MN extent is a multiple of 32: (32 MN elements, K rows,
-// MN/32 chunks), so one box of (32, 32, nchunk) lands as nchunk 4096-byte swizzled chunks.
+// 3-D map of an MN-major operand whose MN extent is a multiple of the 128-byte chunk (c = 32
+// fp32 or 64 bf16 elements): (c MN elements, K rows, MN/c chunks), so one box of
+// (c, c, nchunk) lands as nchunk swizzled chunks of c k-rows x 128 bytes.
 void make_map_mn3d(CUtensorMap* m, const float* base, long long inner, long long outer,
-                   long long row_stride, int nchunk) {
-  cuuint64_t dims[3] = {32, (cuuint64_t)outer, (cuuint64_t)(inner / 32)};
+                   long long row_stride, int nchunk, bool bf16 = false) {
+  const int es = bf16 ? 2 : 4, c = 128 / es;
+  cuuint64_t dims[3] = {(cuuint64_t)c, (cuuint64_t)outer, (cuuint64_t)(inner / c)};
   const long long rs = outer > 1 ? std::max<long long>(row_stride, inner) : inner;
-  cuuint64_t strides[2] = {(cuuint64_t)(rs * 4), 128};
-  cuuint32_t box[3] = {32, 32, (cuuint32_t)nchunk};
+  cuuint64_t strides[2] = {(cuuint64_t)(rs * es), 128};
+  cuuint32_t box[3] = {(cuuint32_t)c, (cuuint32_t)c, (cuuint32_t)nchunk};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = encode_fn()(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                           const_cast<float*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed (" + std::to_string(int(r)) + ")");
@@ -899,10 +1016,10 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo >= 1 && lbo <= 8) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
-bool gemm_view_ok(const MatView& v) {
+bool gemm_view_ok(const MatView& v, bool bf16) {
   if (v.cs != 1) return false;
   if ((reinterpret_cast<uintptr_t>(v.ptr) & 15) != 0) return false;
-  if (v.rows > 1 && (v.rs % 4) != 0) return false;
+  if (v.rows > 1 && (v.rs % (bf16 ? 8 : 4)) != 0) return false;  // 16-byte row pitch (TMA)
   return true;
 }
 
@@ -1019,6 +1136,11 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   GemmLaunch g;
   g.split = split;
   const GemmSpec& s0 = specs[0];
+  g.bf16 = s0.bf16;
+  const bool bf = g.bf16;
+  const int mnc = bf ? 64 : 32, bke = bf ? 64 : 32;  // MN-major chunk / k-block (elements)
+  for (const auto& s : specs)
+    if (s.bf16 != bf) throw std::runtime_error("gemm: mixed storage types in one batch");
   const long long M0 = s0.ta ? s0.a.cols : s0.a.rows;
   const long long N0 = s0.tb ? s0.b.rows : s0.b.cols;
   g.swap = (M0 < 128 && N0 >= 2 * M0);
@@ -1038,7 +1160,7 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   probs.resize(specs.size());
   for (size_t i = 0; i < specs.size(); ++i) {
     const GemmSpec& s = specs[i];
-    if (!gemm_view_ok(s.a) || !gemm_view_ok(s.b))
+    if (!gemm_view_ok(s.a, bf) || !gemm_view_ok(s.b, bf))
       throw std::runtime_error("gemm: operand view is not TMA-compatible");
     const long long M = s.ta ? s.a.cols : s.a.rows;
     const long long K = s.ta ? s.a.rows : s.a.cols;
@@ -1056,24 +1178,26 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
       throw std::runtime_error("gemm: mixed operand majorness in one batch");
     }
     GemmProblem& pr = probs[i];
-    if (rp.mn && rp.inner % 32 == 0 && !g_no_3d) {
-      make_map_mn3d(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, BM / 32);
+    if (rp.mn && rp.inner % mnc == 0 && !g_no_3d) {
+      make_map_mn3d(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, BM / mnc, bf);
       pr.a3d = 1;
     } else {
-      make_map(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, 32, rp.mn ? 32 : BM, rp.mn);
+      make_map(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, rp.mn ? mnc : bke, rp.mn ? bke : BM, rp.mn,
+               false, bf);
     }
-    if (rq.mn && rq.inner % 32 == 0 && !g_no_3d) {
-      make_map_mn3d(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, bnh / 32);
+    if (rq.mn && rq.inner % mnc == 0 && !g_no_3d) {
+      make_map_mn3d(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, bnh / mnc, bf);
       pr.b3d = 1;
     } else {
-      make_map(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, 32, rq.mn ? 32 : bnh, rq.mn);
+      make_map(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, rq.mn ? mnc : bke, rq.mn ? bke : bnh,
+               rq.mn, false, bf);
     }
     pr.P = int(g.swap ? N : M);
     pr.Q = int(g.swap ? M : N);
     pr.K = int(K);
     pr.tiles_p = int((pr.P + pbm - 1) / pbm);
     pr.tiles_q = int((pr.Q + g.bn - 1) / g.bn);
-    pr.kb_total = int((K + BK - 1) / BK);
+    pr.kb_total = int((K + bke - 1) / bke);
     pr.out = s.c;
     pr.out_rs = g.swap ? s.c_cs : s.c_rs;
     pr.out_cs = g.swap ? s.c_rs : s.c_cs;
@@ -1089,14 +1213,14 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     }
     // TMA load map for the epilogue operand (row-major, 16-byte aligned base and pitch)
     auto storable = [&](const float* b, long long rs, long long cs) {
-      return b && cs == 1 && (reinterpret_cast<uintptr_t>(b) & 15) == 0 && (pr.P == 1 || rs % 4 == 0);
+      return b && cs == 1 && (reinterpret_cast<uintptr_t>(b) & 15) == 0 && (pr.P == 1 || rs % (bf ? 8 : 4) == 0);
     };
     for (int e = 0; e < s.n_epi; ++e) {
       if (!epi_needs_other_host(pr.epi[e].op)) continue;
       pr.other_stage = e;
       if (!g_no_tma_store && storable(pr.epi[e].other, pr.epi[e].o_rs, pr.epi[e].o_cs)) {
         store_maps.emplace_back();
-        make_map(&store_maps.back(), pr.epi[e].other, pr.Q, pr.P, pr.epi[e].o_rs, CW, 32, false, true);
+        make_map(&store_maps.back(), pr.epi[e].other, pr.Q, pr.P, pr.epi[e].o_rs, CW, 32, false, true, bf);
         store_idx.push_back({int(i), 1 + kMaxEpi});
         g.other_smem = true;
       }
@@ -1107,9 +1231,10 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     for (int e = 0; e < s.n_epi; ++e) ok = ok && small(pr.epi[e].out_rs) && small(pr.epi[e].out_cs);
     if (!ok) throw std::runtime_error("gemm: output strides exceed 2^31 elements");
     g.flops += 2.0 * double(M) * double(N) * double(K);
-    g.min_bytes += 4.0 * double(M * K + K * N + M * N * (1 + s.n_epi));
+    const double es = bf ? 2.0 : 4.0;
+    g.min_bytes += es * double(M * K + K * N + M * N * (1 + s.n_epi));
     for (int e = 0; e < s.n_epi; ++e)
-      if (s.epi[e].op >= EPI_ADD) g.min_bytes += 4.0 * double(M * N);
+      if (s.epi[e].op >= EPI_ADD) g.min_bytes += es * double(M * N);
   }
   // L2 policy: operands re-read by many tiles and small enough to stay resident are kept
   // (evict_last); large streamed ones (a weight read once per step) and epilogue outputs far
@@ -1170,14 +1295,14 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   g.smem_bytes = smem_for(bn_stage, split, g.odepth, g.stages);
   g.prefetch = g_prefetch >= 0 ? g_prefetch : 0;
   g.threads = threads_for(split);
-  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, split, g.pair);
+  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, split, g.pair, g.bf16);
   // the attribute is per function and launches of one instantiation differ in smem: allow the max
   CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemMax)));
   return g;
 }
 
 void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
-  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair);
+  KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair, g.bf16);
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
   const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4);

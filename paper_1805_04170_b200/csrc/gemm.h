@@ -84,6 +84,7 @@ struct MatView {
 struct GemmSpec {
   MatView a, b;                 // stored operands (before transposition)
   bool ta = false, tb = false;  // MatmulAttrs
+  bool bf16 = false;            // bf16 storage (operands, outputs, epilogue operands)
   float* c = nullptr;           // output M x N
   long long c_rs = 0, c_cs = 1;
   int n_epi = 0;
@@ -95,6 +96,7 @@ struct GemmLaunch {
   bool split = false;           // 3xTF32
   bool p_mn = false, q_mn = false, swap = false;
   bool pair = false;            // CTA-pair (cta_group::2) 256 x 256 tiles
+  bool bf16 = false;            // bf16 storage: kind::f16 MMAs
   int units = 0;                // CTAs launched
   int nprob = 0;
   int threads = 256;
@@ -118,7 +120,7 @@ struct GemmLaunch {
 
 // Whether `spec` can run on the TMA path (16-byte aligned bases and row strides, unit inner
 // strides).  The plan lowering materialises a packed copy of any view that cannot.
-bool gemm_view_ok(const MatView& v);
+bool gemm_view_ok(const MatView& v, bool bf16 = false);
 
 // Builds tensor maps / problem tables (device memory owned by the launch).
 // split = 3xTF32 (fp32-accurate products), else single-pass TF32.

@@ -116,9 +116,10 @@ def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None, precision: int = 0,
     (ms, CUDA events on the stream) is returned."""
     import torch  # plumbing only: device pointers and the current stream
 
+    want = torch.bfloat16 if precision == 2 else torch.float32
     for t in (A, B, C):
-        if t.dtype != torch.float32 or t.dim() != 2 or t.stride(1) != 1:
-            raise TpxError("gemm operands must be 2-D fp32 with unit inner stride")
+        if t.dtype != want or t.dim() != 2 or t.stride(1) != 1:
+            raise TpxError(f"gemm operands must be 2-D {want} with unit inner stride")
     epi = epi or []
     n = len(epi)
     ops = (c_int * max(n, 1))(*[e[0] for e in epi])

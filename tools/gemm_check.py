@@ -18,17 +18,23 @@ from paper_1805_04170_b200 import native  # noqa: E402
 
 def run(M, N, K, ta, tb, epi=None, pad=0, precision=0):
     dev = "cuda"
+    dt = torch.bfloat16 if precision == 2 else torch.float32
     g = torch.Generator(device=dev).manual_seed(M * 7 + N * 3 + K)
-    A = torch.rand((K, M) if ta else (M, K), device=dev, generator=g) * 2 - 1
-    B = torch.rand((N, K) if tb else (K, N), device=dev, generator=g) * 2 - 1
-    if pad:
-        A = torch.nn.functional.pad(A, (0, pad))[:, : A.shape[1]]
-    C = torch.full((M, N), float("nan"), device=dev)
+    def padded(t):  # 16-byte row pitch (TMA), as the executor's buffers have
+        al = 16 // t.element_size()
+        cols = t.shape[1]
+        if cols % al == 0 and not pad:
+            return t
+        return torch.nn.functional.pad(t, (0, (-cols) % al + pad))[:, :cols]
+
+    A = padded((torch.rand((K, M) if ta else (M, K), device=dev, generator=g) * 2 - 1).to(dt))
+    B = padded((torch.rand((N, K) if tb else (K, N), device=dev, generator=g) * 2 - 1).to(dt))
+    C = padded(torch.full((M, N), float("nan"), device=dev, dtype=dt))
     outs = []
     if epi:
         for op in epi:
-            outs.append(torch.full((M, N), float("nan"), device=dev))
-    W = torch.rand((M, N), device=dev, generator=g) * 2 - 1
+            outs.append(padded(torch.full((M, N), float("nan"), device=dev, dtype=dt)))
+    W = padded((torch.rand((M, N), device=dev, generator=g) * 2 - 1).to(dt))
     native.gemm(A, B, ta, tb, C, epi=[(op, 0.01, W if op >= 4 else None, o) for op, o in zip(epi or [], outs)],
                 precision=precision)
     torch.cuda.synchronize()
@@ -37,6 +43,8 @@ def run(M, N, K, ta, tb, epi=None, pad=0, precision=0):
     res = [err]
     prev = ref
     for op, o in zip(epi or [], outs):
+        if precision == 2:
+            prev = prev.to(torch.bfloat16).double()  # each stage reads the stored (bf16) value
         if op == 1:
             prev = torch.tanh(prev)
         elif op == 2:
@@ -54,15 +62,16 @@ def run(M, N, K, ta, tb, epi=None, pad=0, precision=0):
 
 
 def bench(M, N, K, ta, tb, iters=20, precision=0, epi=None):
-    A = torch.rand((K, M) if ta else (M, K), device="cuda")
-    B = torch.rand((N, K) if tb else (K, N), device="cuda")
-    C = torch.empty((M, N), device="cuda")
-    W = torch.rand((M, N), device="cuda")
-    outs = [torch.empty((M, N), device="cuda") for _ in (epi or [])]
+    dt = torch.bfloat16 if precision == 2 else torch.float32
+    A = torch.rand((K, M) if ta else (M, K), device="cuda").to(dt)
+    B = torch.rand((N, K) if tb else (K, N), device="cuda").to(dt)
+    C = torch.empty((M, N), device="cuda", dtype=dt)
+    W = torch.rand((M, N), device="cuda").to(dt)
+    outs = [torch.empty((M, N), device="cuda", dtype=dt) for _ in (epi or [])]
     e = [(op, 0.01, W if op >= 4 else None, o) for op, o in zip(epi or [], outs)]
     ms = native.gemm(A, B, ta, tb, C, epi=e, precision=precision, warmup=3, iters=iters)
     tf = 2 * M * N * K / ms / 1e9
-    nb = 4 * (M * K + K * N + M * N * (1 + len(epi or [])) + sum(M * N for op in (epi or []) if op >= 4))
+    nb = (2 if precision == 2 else 4) * (M * K + K * N + M * N * (1 + len(epi or [])) + sum(M * N for op in (epi or []) if op >= 4))
     return ms, tf, nb / ms / 1e6
 
 
@@ -130,7 +139,19 @@ def main():
     errs = run(512, 512, 256, False, False, epi=[1, 2], precision=1)
     good = all(e <= 5e-6 for e in errs)
     ok &= good
-    print(f"{'ok ' if good else 'BAD'} 3xTF32 epilogue [1,2] err={errs}")
+    print(f"{'ok ' if good else 'BAD'} 3xTF32 epilogue [1,2] err={errs}")    # bf16 storage (kind::f16): products of bf16 operands in fp32, outputs rounded to bf16
+    for c in cases:
+        errs = run(*c, precision=2)
+        good = all(e <= 8e-3 for e in errs)
+        ok &= good
+        print(f"{'ok ' if good else 'BAD'} bf16 M,N,K,ta,tb={c} err={errs}")
+    for epi in ([1, 2], [3, 6]):
+        for c in [(512, 512, 256, False, False), (256, 512, 512, True, False), (32, 512, 512, False, False)]:
+            errs = run(*c, epi=epi, precision=2)
+            good = all(e <= 8e-3 for e in errs)
+            ok &= good
+            print(f"{'ok ' if good else 'BAD'} bf16 epilogue {epi} {c} err={errs}")
+
     if "--bench" in sys.argv:
         L = native.lib()
 
@@ -146,6 +167,10 @@ def main():
                        ((4096, 4096, 4096, False, False), None), ((8192, 8192, 8192, False, True), None)]:
             ms, tf, gb = med(c, epi)
             print(f"bench {c} epi={epi}: {ms:.3f} ms  {tf:.1f} TFLOP/s  {gb:.0f} GB/s(min bytes)")
+        for c, epi in [((512, 8192, 8192, False, False), [1]), ((512, 8192, 8192, False, True), [2]),
+                       ((8192, 8192, 512, True, False), [3, 6]), ((8192, 8192, 8192, False, True), None)]:
+            ms, tf, gb = sorted(bench(*c, epi=epi, precision=2) for _ in range(5))[2]
+            print(f"bench bf16 {c} epi={epi}: {ms:.3f} ms  {tf:.1f} TFLOP/s  {gb:.0f} GB/s(min bytes)")
         # interleaved A/B knob experiments: (knob, value) pairs, baseline (0-reset) between
         shapes = [((512, 8192, 8192, False, False), None), ((512, 8192, 8192, False, True), None),
                   ((8192, 8192, 512, True, False), [3, 6]), ((64, 8192, 8192, False, False), None),
