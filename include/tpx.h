@@ -52,6 +52,7 @@ typedef struct tpx_stats {
   int64_t device_bytes;           /* HBM arena bytes allocated for node values           */
   double gemm_flops;              /* 2*M*N*K over this rank's matmul sub-ops             */
   double gemm_min_bytes;          /* operand + output bytes of those GEMMs (read once)   */
+  int64_t storage_bytes;          /* bytes per stored element: 4 (fp32) or 2 (bf16 plan)  */
 } tpx_stats;
 
 const char* tpx_last_error(void);
@@ -98,7 +99,9 @@ int tpx_init_inputs(tpx_plan* plan, uint64_t seed);
 int tpx_node_elements(const tpx_plan* plan, const char* node_id, int64_t* n);
 int tpx_write_node(tpx_plan* plan, const char* node_id, const double* src, int64_t n);
 int tpx_read_node(tpx_plan* plan, const char* node_id, double* dst, int64_t n);
-/* fp32 host <-> device for a node (pinned buffers give async copies on the plan stream). */
+/* Raw storage-type host <-> device for a node: n elements of the plan's storage type (fp32, or
+ * bf16 for dtype_bytes-2 plans; tpx_stats.storage_bytes), pinned buffers give async copies on
+ * the plan stream.  (tpx_read_node / tpx_write_node convert to / from fp64.) */
 int tpx_write_node_f32(tpx_plan* plan, const char* node_id, const float* src, int64_t n);
 int tpx_read_node_f32(tpx_plan* plan, const char* node_id, float* dst, int64_t n);
 /* Device address + element strides of a node value (for zero-copy interop). */

@@ -118,6 +118,7 @@ TPX_API int tpx_plan_stats(const tpx_plan* plan, tpx_stats* out) {
     s.device_bytes = int64_t(P.arena_used);
     s.gemm_flops = P.gemm_flops;
     s.gemm_min_bytes = P.gemm_min_bytes;
+    s.storage_bytes = P.esize;
     *out = s;
   });
 }

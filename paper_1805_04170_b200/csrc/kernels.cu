@@ -4,6 +4,8 @@
 // moves float4s.
 #include "kernels.h"
 
+#include <cuda_bf16.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -11,6 +13,60 @@
 #include "util.h"
 
 namespace tpx {
+
+namespace {
+// ---- storage element access: T = float or __nv_bfloat16 (arithmetic is always fp32)
+template <class T>
+__device__ __forceinline__ float eld(const T* p) {
+  if constexpr (sizeof(T) == 2) return __bfloat162float(__ldg(p));
+  else return __ldg(p);
+}
+template <class T>
+__device__ __forceinline__ float eldv(const T* p) {  // plain (coherent) load, for accumulate
+  if constexpr (sizeof(T) == 2) return __bfloat162float(*p);
+  else return *p;
+}
+template <class T>
+__device__ __forceinline__ void est(T* p, float v) {
+  if constexpr (sizeof(T) == 2) *p = __float2bfloat16_rn(v);
+  else *p = v;
+}
+// 4 consecutive elements (16 B fp32 / 8 B bf16, aligned)
+template <class T>
+__device__ __forceinline__ float4 eld4(const T* p) {
+  if constexpr (sizeof(T) == 2) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  } else {
+    return __ldg(reinterpret_cast<const float4*>(p));
+  }
+}
+template <class T>
+__device__ __forceinline__ float4 eld4v(const T* p) {
+  if constexpr (sizeof(T) == 2) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  } else {
+    return *reinterpret_cast<const float4*>(p);
+  }
+}
+template <class T>
+__device__ __forceinline__ void est4(T* p, float4 v) {
+  if constexpr (sizeof(T) == 2) {
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&a);
+    u.y = *reinterpret_cast<const uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+  } else {
+    *reinterpret_cast<float4*>(p) = v;
+  }
+}
+}  // namespace
 
 namespace {
 
@@ -77,6 +133,7 @@ __device__ __forceinline__ float nary_apply(int op, int nin, const float* v, flo
   }
 }
 
+template <class T>
 __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restrict__ ds, int n) {
   const int di = find_desc(&ds[0].d.tile_begin, sizeof(NaryDev), n, blockIdx.x);
   const NaryDev& D = ds[di];
@@ -95,20 +152,20 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
     const int64_t t = r / d.shape[2];
     const int64_t i1 = t % d.shape[1];
     const int64_t i0 = t / d.shape[1];
-    float* out = d.out + i0 * d.out_st[0] + i1 * d.out_st[1] + i2 * d.out_st[2];
-    const float* in[kMaxIn];
+    T* out = reinterpret_cast<T*>(d.out) + i0 * d.out_st[0] + i1 * d.out_st[1] + i2 * d.out_st[2];
+    const T* in[kMaxIn];
 #pragma unroll
     for (int k = 0; k < kMaxIn; ++k)
-      if (k < nin) in[k] = d.in[k] + i0 * d.in_st[k][0] + i1 * d.in_st[k][1] + i2 * d.in_st[k][2];
+      if (k < nin) in[k] = reinterpret_cast<const T*>(d.in[k]) + i0 * d.in_st[k][0] + i1 * d.in_st[k][1] + i2 * d.in_st[k][2];
     if (d.vec == 4) {
       for (int64_t c = c0 + lane; c < c1; c += cstep) {
         float4 v[kMaxIn];
 #pragma unroll
         for (int k = 0; k < kMaxIn; ++k)
-          if (k < nin) v[k] = __ldg(reinterpret_cast<const float4*>(in[k]) + c);
+          if (k < nin) v[k] = eld4(in[k] + 4 * c);
         float4 o;
         if (op == NARY_ACC) {
-          o = reinterpret_cast<float4*>(out)[c];
+          o = eld4v(out + 4 * c);
           o.x += v[0].x; o.y += v[0].y; o.z += v[0].z; o.w += v[0].w;
         } else {
           float a[kMaxIn];
@@ -125,16 +182,16 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
           for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? v[k].w : 0.f;
           o.w = nary_apply(op, nin, a, d.scale);
         }
-        reinterpret_cast<float4*>(out)[c] = o;
+        est4(out + 4 * c, o);
       }
     } else {
       const int64_t os = d.out_st[3];
       for (int64_t c = c0 + lane; c < c1; c += cstep) {
         float a[kMaxIn];
 #pragma unroll
-        for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? __ldg(in[k] + c * d.in_st[k][3]) : 0.f;
-        if (op == NARY_ACC) out[c * os] += a[0];
-        else out[c * os] = nary_apply(op, nin, a, d.scale);
+        for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? eld(in[k] + c * d.in_st[k][3]) : 0.f;
+        if (op == NARY_ACC) est(out + c * os, eldv(out + c * os) + a[0]);
+        else est(out + c * os, nary_apply(op, nin, a, d.scale));
       }
     }
   }
@@ -158,6 +215,7 @@ __device__ __forceinline__ float seeded_value(uint64_t state0, uint64_t flat) {
   return float(v);  // round-to-nearest fp64 -> fp32
 }
 
+template <class T>
 __global__ void __launch_bounds__(kThreads) init_kernel(const InitDev* __restrict__ ds, int n) {
   const int di = find_desc(&ds[0].d.tile_begin, sizeof(InitDev), n, blockIdx.x);
   const InitDev& D = ds[di];
@@ -175,17 +233,20 @@ __global__ void __launch_bounds__(kThreads) init_kernel(const InitDev* __restric
     const uint64_t rowflat =
         ((uint64_t(d.lo[0] + i0) * d.full[1] + uint64_t(d.lo[1] + i1)) * d.full[2] +
          uint64_t(d.lo[2] + i2)) * d.full[3] + uint64_t(d.lo[3]);
-    float* out = d.out + r * d.ext[3];
-    for (int64_t c = c0 + lane; c < c1; c += 32) out[c] = seeded_value(d.state0, rowflat + uint64_t(c));
+    T* out = reinterpret_cast<T*>(d.out) + r * d.ext[3];
+    // fp64 -> fp32 (round to nearest) -> storage type (bf16: round to nearest even)
+    for (int64_t c = c0 + lane; c < c1; c += 32) est(out + c, seeded_value(d.state0, rowflat + uint64_t(c)));
   }
 }
 
 // ---------------------------------------------------------------- conv (direct)
 
+template <class T>
 __device__ __forceinline__ float at4(const StridedView& v, int64_t a, int64_t b, int64_t c, int64_t d) {
-  return __ldg(v.ptr + a * v.st[0] + b * v.st[1] + c * v.st[2] + d * v.st[3]);
+  return eld(reinterpret_cast<const T*>(v.ptr) + a * v.st[0] + b * v.st[1] + c * v.st[2] + d * v.st[3]);
 }
 
+template <class T>
 __global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restrict__ ds, int n) {
   const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
   const ConvDesc& d = ds[di];
@@ -203,13 +264,13 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restri
     const int64_t ci = d.a.shape[1], fh = d.b.shape[2], fw = d.b.shape[3];
     for (int64_t c = 0; c < ci; ++c)
       for (int64_t u = 0; u < fh; ++u)
-        for (int64_t v = 0; v < fw; ++v) acc = fmaf(at4(d.a, o0, c, o2 + u, o3 + v), at4(d.b, o1, c, u, v), acc);
+        for (int64_t v = 0; v < fw; ++v) acc = fmaf(at4<T>(d.a, o0, c, o2 + u, o3 + v), at4<T>(d.b, o1, c, u, v), acc);
   } else if (d.mode == CONV_GRAD_W) {
     // A (n,ci,h,w) x G (n,co,ho,wo) -> (co,ci,fh,fw)
     const int64_t nb = d.a.shape[0], ho = d.b.shape[2], wo = d.b.shape[3];
     for (int64_t b = 0; b < nb; ++b)
       for (int64_t y = 0; y < ho; ++y)
-        for (int64_t x = 0; x < wo; ++x) acc = fmaf(at4(d.a, b, o1, y + o2, x + o3), at4(d.b, b, o0, y, x), acc);
+        for (int64_t x = 0; x < wo; ++x) acc = fmaf(at4<T>(d.a, b, o1, y + o2, x + o3), at4<T>(d.b, b, o0, y, x), acc);
   } else {
     // G (n,co,ho,wo) x K (co,ci,fh,fw) -> (n,ci,ho+fh-1,wo+fw-1), bounds-checked taps
     const int64_t co = d.a.shape[1], ho = d.a.shape[2], wo = d.a.shape[3];
@@ -221,17 +282,18 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restri
         for (int64_t v = 0; v < fw; ++v) {
           const int64_t xx = o3 - v;
           if (xx < 0 || xx >= wo) continue;
-          acc = fmaf(at4(d.a, o0, o, yy, xx), at4(d.b, o, o1, u, v), acc);
+          acc = fmaf(at4<T>(d.a, o0, o, yy, xx), at4<T>(d.b, o, o1, u, v), acc);
         }
       }
   }
-  d.out[e] = acc;
+  est(reinterpret_cast<T*>(d.out) + e, acc);
 }
 
 // im2col / col2im of the tensor-core conv lowering: one warp per output row (lanes over x), so
 // reads and writes are coalesced and the index decomposition is paid once per row.
 constexpr int kRowsPerWarp = 8;
 
+template <class T>
 __global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __restrict__ ds, int n) {
   const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
   const ConvDesc& d = ds[di];
@@ -249,13 +311,13 @@ __global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __re
     const int R = NB * Yo, nblk = (R + kRowsPerBlock - 1) / kRowsPerBlock;
     const int k = tile / nblk, rb = tile - k * nblk;
     const int v = k % V, u = (k / V) % U, c = k / (U * V);
-    const float* src0 = d.a.ptr + c * d.a.st[1] + u * d.a.st[2] + v * d.a.st[3];
-    float* dst0 = d.out + int64_t(k) * pitch;
+    const T* src0 = reinterpret_cast<const T*>(d.a.ptr) + c * d.a.st[1] + u * d.a.st[2] + v * d.a.st[3];
+    T* dst0 = reinterpret_cast<T*>(d.out) + int64_t(k) * pitch;
     const int r0 = rb * kRowsPerBlock + warp * kRowsPerWarp;
     for (int x0 = 0; x0 < Xo; x0 += 32) {
       const int x = x0 + lane;
       float val[kRowsPerWarp];
-      float* dst[kRowsPerWarp];
+      T* dst[kRowsPerWarp];
 #pragma unroll
       for (int j = 0; j < kRowsPerWarp; ++j) {
         const int r = r0 + j;
@@ -263,13 +325,13 @@ __global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __re
         val[j] = 0.f;
         if (r < R && x < Xo) {
           const int nb = r / Yo, y = r - nb * Yo;
-          val[j] = __ldg(src0 + nb * d.a.st[0] + y * d.a.st[2] + x * d.a.st[3]);
+          val[j] = eld(src0 + nb * d.a.st[0] + y * d.a.st[2] + x * d.a.st[3]);
           dst[j] = dst0 + nb * img + y * Xo + x;
         }
       }
 #pragma unroll
       for (int j = 0; j < kRowsPerWarp; ++j)
-        if (dst[j]) *dst[j] = val[j];
+        if (dst[j]) est(dst[j], val[j]);
     }
   } else {
     // block = ((nb, c), chunk of kRowsPerBlock y rows); per output element
@@ -280,8 +342,8 @@ __global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __re
     const int nblk = (H + kRowsPerBlock - 1) / kRowsPerBlock;
     const int nc = tile / nblk, yb = tile - nc * nblk;
     const int c = nc % C, nb = nc / C;
-    const float* col = d.a.ptr + int64_t(nb) * img + int64_t(c * U * V) * pitch;
-    float* out = d.out + int64_t(nc) * H * W;
+    const T* col = reinterpret_cast<const T*>(d.a.ptr) + int64_t(nb) * img + int64_t(c * U * V) * pitch;
+    T* out = reinterpret_cast<T*>(d.out) + int64_t(nc) * H * W;
     const int y0 = yb * kRowsPerBlock + warp * kRowsPerWarp;
     for (int j = 0; j < kRowsPerWarp; ++j) {
       const int y = y0 + j;
@@ -291,14 +353,14 @@ __global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __re
         for (int u = 0; u < U; ++u) {
           const int yy = y - u;
           if (yy < 0 || yy >= Yo) continue;
-          const float* crow = col + int64_t(u * V) * pitch + yy * Xo;
+          const T* crow = col + int64_t(u * V) * pitch + yy * Xo;
 #pragma unroll 4
           for (int vv = 0; vv < V; ++vv) {
             const int xx = x - vv;
-            if (xx >= 0 && xx < Xo) acc += __ldg(crow + int64_t(vv) * pitch + xx);
+            if (xx >= 0 && xx < Xo) acc += eld(crow + int64_t(vv) * pitch + xx);
           }
         }
-        out[int64_t(y) * W + x] = acc;
+        est(out + int64_t(y) * W + x, acc);
       }
     }
   }
@@ -324,7 +386,7 @@ bool StridedView::contiguous() const {
   return true;
 }
 
-NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView>& ins, float scale) {
+NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView>& ins, float scale, int esize) {
   if (ins.empty() || int(ins.size()) > kMaxIn) fail("nary: bad operand count");
   NaryDesc d;
   std::memset(&d, 0, sizeof d);
@@ -379,11 +441,12 @@ NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView
   }
   d.out = out.ptr;
   for (size_t k = 0; k < ins.size(); ++k) d.in[k] = ins[k].ptr;
-  // float4 path: unit inner stride everywhere, inner extent % 4, 16B-aligned rows.
-  bool v4 = d.shape[3] % 4 == 0 && d.out_st[3] == 1 && (reinterpret_cast<uintptr_t>(d.out) & 15) == 0;
+  // 4-wide path: unit inner stride everywhere, inner extent % 4, rows aligned to 4 elements.
+  const uintptr_t al = uintptr_t(4 * esize - 1);
+  bool v4 = d.shape[3] % 4 == 0 && d.out_st[3] == 1 && (reinterpret_cast<uintptr_t>(d.out) & al) == 0;
   for (int i = 0; i < 3 && v4; ++i) v4 = d.out_st[i] % 4 == 0;
   for (size_t k = 0; k < ins.size() && v4; ++k) {
-    v4 = d.in_st[k][3] == 1 && (reinterpret_cast<uintptr_t>(d.in[k]) & 15) == 0;
+    v4 = d.in_st[k][3] == 1 && (reinterpret_cast<uintptr_t>(d.in[k]) & al) == 0;
     for (int i = 0; i < 3 && v4; ++i) v4 = d.in_st[k][i] % 4 == 0;
   }
   d.vec = v4 ? 4 : 1;
@@ -404,7 +467,7 @@ void nary_prepare(NaryBatch& b) {
     tiles += ((rows + t.rpt - 1) / t.rpt) * t.n_col_chunks;
     dev[i] = NaryDev{d, t.rows, t.inner, t.rpt, t.col_chunk, t.n_col_chunks};
     const double elems = double(d.units) * d.vec;
-    b.bytes += 4.0 * elems * (d.nin + 1 + (d.op == NARY_ACC ? 1 : 0));
+    b.bytes += (b.bf16 ? 2.0 : 4.0) * elems * (d.nin + 1 + (d.op == NARY_ACC ? 1 : 0));
   }
   b.tiles = tiles;
   upload(dev, &b.d_descs);
@@ -412,8 +475,12 @@ void nary_prepare(NaryBatch& b) {
 
 void nary_run(const NaryBatch& b, cudaStream_t s) {
   if (!b.tiles) return;
-  nary_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
-                                                     int(b.descs.size()));
+  if (b.bf16)
+    nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
+                                                                      int(b.descs.size()));
+  else
+    nary_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
+                                                              int(b.descs.size()));
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -448,8 +515,12 @@ void init_prepare(InitBatch& b) {
 
 void init_run(const InitBatch& b, cudaStream_t s) {
   if (!b.tiles) return;
-  init_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const InitDev*>(b.d_descs),
-                                                     int(b.descs.size()));
+  if (b.bf16)
+    init_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const InitDev*>(b.d_descs),
+                                                                      int(b.descs.size()));
+  else
+    init_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const InitDev*>(b.d_descs),
+                                                              int(b.descs.size()));
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -483,12 +554,12 @@ void conv_prepare(ConvBatch& b) {
 
 void conv_run(const ConvBatch& b, cudaStream_t s) {
   if (!b.tiles) return;
-  if (b.move)
-    convmove_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const ConvDesc*>(b.d_descs),
-                                                           int(b.descs.size()));
-  else
-    conv_kernel<<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const ConvDesc*>(b.d_descs),
-                                                       int(b.descs.size()));
+  const ConvDesc* ds = static_cast<const ConvDesc*>(b.d_descs);
+  const int nd = int(b.descs.size());
+  if (b.move && b.bf16) convmove_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
+  else if (b.move) convmove_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
+  else if (b.bf16) conv_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
+  else conv_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
   CUDA_CHECK(cudaGetLastError());
 }
 

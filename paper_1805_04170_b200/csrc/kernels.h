@@ -26,7 +26,8 @@ enum NaryOp : int {
   NARY_ACC = 6,    // out += in0
 };
 
-// A strided fp32 view (element strides), rank <= 4.
+// A strided view (element strides), rank <= 4.  `ptr` is an opaque device address; the element
+// type (fp32 or bf16) is the plan's storage type.
 struct StridedView {
   float* ptr = nullptr;
   int rank = 0;
@@ -55,6 +56,7 @@ struct NaryDesc {
 };
 
 struct NaryBatch {
+  bool bf16 = false;  // storage type of every operand (arithmetic is fp32)
   std::vector<NaryDesc> descs;
   void* d_descs = nullptr;
   int64_t tiles = 0;
@@ -63,7 +65,7 @@ struct NaryBatch {
 
 // Build a descriptor: out[i] = op(in_0[i], ...), all views of equal shape.
 NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView>& ins,
-                   float scale = 0.f);
+                   float scale = 0.f, int esize = 4);
 void nary_prepare(NaryBatch& b);  // uploads descriptor table
 void nary_run(const NaryBatch& b, cudaStream_t s);
 void nary_free(NaryBatch& b);
@@ -80,6 +82,7 @@ struct InitDesc {
 };
 
 struct InitBatch {
+  bool bf16 = false;  // storage type written (seeded fp64 -> fp32 -> bf16, round to nearest)
   std::vector<InitDesc> descs;
   void* d_descs = nullptr;
   int64_t tiles = 0;
@@ -116,6 +119,7 @@ struct ConvBatch {
   int64_t tiles = 0;
   double flops = 0;
   bool move = false;  // im2col / col2im batch (d.n counts rows) rather than direct conv
+  bool bf16 = false;  // storage type
 };
 void conv_prepare(ConvBatch& b);
 void conv_run(const ConvBatch& b, cudaStream_t s);

@@ -14,6 +14,16 @@ namespace tpx {
 namespace {
 
 constexpr size_t kAlign = 256;
+
+// Storage element size of the plan being lowered / read / written (4 = fp32, 2 = bf16).  Set by
+// the entry points from PlanRt::esize; one host thread drives a plan at a time.
+thread_local int g_es = 4;
+inline float* eoff(float* p, int64_t elems) {
+  return reinterpret_cast<float*>(reinterpret_cast<char*>(p) + elems * g_es);
+}
+inline NaryDesc ndesc(int op, const StridedView& out, const std::vector<StridedView>& ins, float scale = 0.f) {
+  return nary_desc(op, out, ins, scale, g_es);
+}
 constexpr uintptr_t kFakeBase = uintptr_t(1) << 40;  // dry-run arena base (256-aligned)
 
 StridedView contiguous_view(float* ptr, const Shape& s) {
@@ -38,7 +48,7 @@ StridedView subview(const StridedView& v, const Region& vreg, const Region& sub)
     off += (sub.b[size_t(i)][0] - vreg.b[size_t(i)][0]) * v.st[i];
     o.shape[i] = sub.b[size_t(i)][1] - sub.b[size_t(i)][0];
   }
-  o.ptr = v.ptr + off;
+  o.ptr = eoff(v.ptr, off);
   return o;
 }
 
@@ -99,7 +109,7 @@ struct Lowerer {
   StridedView alloc(const Shape& s) {
     int64_t n = 1;
     for (auto e : s) n *= e;
-    return contiguous_view(alloc_bytes(size_t(n) * 4), s);
+    return contiguous_view(alloc_bytes(size_t(n) * size_t(g_es)), s);
   }
 
   int rank_of(int dev) const { return P.dev_rank[size_t(dev)]; }
@@ -235,7 +245,7 @@ struct Lowerer {
       const double M = double(op.ta ? s.a.cols : s.a.rows), K = double(op.ta ? s.a.rows : s.a.cols);
       const double N = double(op.tb ? s.b.rows : s.b.cols);
       P.gemm_flops += 2.0 * M * N * K;
-      P.gemm_min_bytes += 4.0 * (M * K + K * N + M * N);
+      P.gemm_min_bytes += double(g_es) * (M * K + K * N + M * N);
     } else if (op.kind == OpKind::elementwise) {
       std::vector<StridedView> ins;
       for (int s : n.sources) ins.push_back(value(s));
@@ -247,7 +257,7 @@ struct Lowerer {
         case EwFn::pointwise_fn: code = NARY_TANH; break;
         case EwFn::pointwise_fn_grad: code = NARY_DTANH; break;
       }
-      o_ew.descs.push_back(nary_desc(code, out, ins, float(op.scale)));
+      o_ew.descs.push_back(ndesc(code, out, ins, float(op.scale)));
     } else {
       ConvDesc d;
       std::memset(&d, 0, sizeof d);
@@ -280,7 +290,8 @@ struct Lowerer {
     m.cs = 1;
     return gemm_view_ok(m);
   }
-  static int64_t pitch4(int64_t n) { return (n + 3) / 4 * 4; }  // 16-byte fp32 rows (TMA)
+  // 16-byte rows (TMA): 4 fp32 or 8 bf16 elements
+  static int64_t pitch4(int64_t n) { const int64_t a = 16 / g_es; return (n + a - 1) / a * a; }
 
   // Copy of a rank-4 view into fresh storage whose last `merge` dims form dense rows padded to
   // 16 bytes: returns the copy with the original shape (pre class, before the op's compute).
@@ -291,14 +302,14 @@ struct Lowerer {
     for (int i = 4 - merge; i < 4; ++i) inner *= v.shape[i];
     const int64_t rows = v.elements() / std::max<int64_t>(inner, 1), ld = pitch4(inner);
     StridedView t = v;
-    t.ptr = alloc_bytes(size_t(rows * ld) * 4);
+    t.ptr = alloc_bytes(size_t(rows * ld) * size_t(g_es));
     int64_t st = 1;
     for (int i = 3; i >= 0; --i) {
       t.st[i] = st;
       st *= v.shape[i];
       if (i == 4 - merge) st = ld;
     }
-    o_pre.descs.push_back(nary_desc(NARY_COPY, t, {v}));
+    o_pre.descs.push_back(ndesc(NARY_COPY, t, {v}));
     return t;
   }
 
@@ -341,7 +352,7 @@ struct Lowerer {
       }
       auto hit = col_cache.find(key);
       if (hit != col_cache.end()) return hit->second;
-      float* t = alloc_bytes(size_t(K * pitch) * 4);  // padding columns stay 0 (zeroed arena)
+      float* t = alloc_bytes(size_t(K * pitch) * size_t(g_es));  // padding columns stay 0 (zeroed arena)
       col_cache[key] = t;
       ConvDesc d;
       std::memset(&d, 0, sizeof d);
@@ -377,8 +388,8 @@ struct Lowerer {
       for (int64_t i = 0; i < NB; ++i) {
         GemmSpec s;
         s.a = km;
-        s.b = MatView{col + i * img, K, YX, ld, 1};  // [K x YX] row-major (MN-major operand)
-        s.c = out.ptr + i * O * YX;
+        s.b = MatView{eoff(col, i * img), K, YX, ld, 1};  // [K x YX] row-major (MN-major operand)
+        s.c = eoff(out.ptr, i * O * YX);
         s.c_rs = YX;
         specs.push_back(s);
       }
@@ -393,14 +404,14 @@ struct Lowerer {
       // G[n, o, y, x] -> Gp[o][(n, img-strided y, x)] (padding columns stay 0: zeroed arena)
       if (!o_pre.descs.empty() && o_pre_op != op.id) flush();
       o_pre_op = op.id;
-      float* gp = alloc_bytes(size_t(O * ld) * 4);
+      float* gp = alloc_bytes(size_t(O * ld) * size_t(g_es));
       StridedView src = b, dst = b;
       src.shape[0] = O; src.shape[1] = NB;  // permuted view of G: (o, n, y, x)
       src.st[0] = b.st[1]; src.st[1] = b.st[0];
       dst.ptr = gp;
       dst.shape[0] = O; dst.shape[1] = NB;
       dst.st[0] = ld; dst.st[1] = img; dst.st[2] = Xo; dst.st[3] = 1;
-      o_pre.descs.push_back(nary_desc(NARY_COPY, dst, {src}));
+      o_pre.descs.push_back(ndesc(NARY_COPY, dst, {src}));
       GemmSpec s;  // contraction over all images' (padded) columns; pads are 0 in both operands
       s.a = MatView{gp, O, NB * img, ld, 1};
       s.b = MatView{col, K, NB * img, ld, 1};
@@ -420,13 +431,13 @@ struct Lowerer {
             (reinterpret_cast<uintptr_t>(g.ptr) & 15) == 0))
         g = padded_copy(a, 2, op.id);
       const int64_t img = pitch4(YX), ld = pitch4(NB * img);
-      float* dcol = alloc_bytes(size_t(K * ld) * 4);
+      float* dcol = alloc_bytes(size_t(K * ld) * size_t(g_es));
       for (int64_t i = 0; i < NB; ++i) {
         GemmSpec s;
         s.a = km;                                                // Kmat [o, cuv], used transposed
         s.ta = true;
-        s.b = MatView{g.ptr + i * g.st[0], O, YX, g.st[1], 1};  // G_n [o, yx] (K x N)
-        s.c = dcol + i * img;
+        s.b = MatView{eoff(g.ptr, i * g.st[0]), O, YX, g.st[1], 1};  // G_n [o, yx] (K x N)
+        s.c = eoff(dcol, i * img);
         s.c_rs = ld;
         specs.push_back(s);
       }
@@ -453,10 +464,10 @@ struct Lowerer {
     // columns lie outside the tensor map and are never read).
     const StridedView& v = value(node);
     if (v.rank != 2) fail("matmul operand is not rank 2");
-    const int64_t rows = v.shape[0], cols = v.shape[1], ld = (cols + 3) / 4 * 4;
+    const int64_t rows = v.shape[0], cols = v.shape[1], ld = pitch4(cols);
     StridedView t = alloc({rows, ld});
     t.shape[1] = cols;
-    o_pre.descs.push_back(nary_desc(NARY_COPY, t, {v}));
+    o_pre.descs.push_back(ndesc(NARY_COPY, t, {v}));
     return t;
   }
 
@@ -513,7 +524,7 @@ struct Lowerer {
 
   // ------------------------------------------------------------ conversions
   void copy_into(const StridedView& dst, const StridedView& src) {
-    o_copy.descs.push_back(nary_desc(NARY_COPY, dst, {src}));
+    o_copy.descs.push_back(ndesc(NARY_COPY, dst, {src}));
   }
 
   void lower_fetch_or_slice(int ni) {
@@ -553,14 +564,14 @@ struct Lowerer {
       return;
     }
     // cross-rank (or forced) transfer through NCCL
-    const size_t bytes = size_t(n.region.volume()) * 4;
+    const size_t bytes = size_t(n.region.volume()) * size_t(g_es);
     if (src_mine) {
       need(src, C_PACK);
       const StridedView sv = subview(value(src), sn.region, n.region);
       const float* sp = sv.ptr;
       if (!sv.contiguous()) {
         const StridedView st = alloc(n.region.shape());
-        o_pack.descs.push_back(nary_desc(NARY_COPY, st, {sv}));
+        o_pack.descs.push_back(ndesc(NARY_COPY, st, {sv}));
         sp = st.ptr;
       }
       o_xchg.x.push_back(Xfer{rank_of(n.device), true, const_cast<float*>(sp), bytes, ni});
@@ -619,7 +630,7 @@ struct Lowerer {
     // Sum in source order (execgraph.cpp:264-282 fixes that order).  More than 8 partials
     // (k > 3) continue as out = out + next 7 in a following launch.
     size_t i = std::min(ins.size(), size_t(kMaxIn));
-    o_reduce.descs.push_back(nary_desc(i == 1 ? NARY_COPY : NARY_SUM, out,
+    o_reduce.descs.push_back(ndesc(i == 1 ? NARY_COPY : NARY_SUM, out,
                                        std::vector<StridedView>(ins.begin(), ins.begin() + long(i))));
     while (i < ins.size()) {
       produced(ni, C_REDUCE);
@@ -627,7 +638,7 @@ struct Lowerer {
       const size_t j = std::min(ins.size(), i + kMaxIn - 1);
       std::vector<StridedView> chunk{out};
       chunk.insert(chunk.end(), ins.begin() + long(i), ins.begin() + long(j));
-      o_reduce.descs.push_back(nary_desc(NARY_SUM, out, chunk));
+      o_reduce.descs.push_back(ndesc(NARY_SUM, out, chunk));
       i = j;
     }
     produced(ni, C_REDUCE);
@@ -769,7 +780,7 @@ struct Lowerer {
           const int e = pc.second;
           const int sn = src_h[size_t(e)];
           const PlanNode& snode = pl.nodes[size_t(sn)];
-          const size_t bytes = size_t(pc.first.volume()) * 4;
+          const size_t bytes = size_t(pc.first.volume()) * size_t(g_es);
           const bool remote = rank_of(e) != rank_of(d) || (force_xchg && e != d);
           if (e != d) P.carry_bytes += int64_t(bytes);
           if (!remote) {
@@ -783,7 +794,7 @@ struct Lowerer {
             const float* sp = sv.ptr;
             if (!sv.contiguous()) {
               const StridedView st = alloc(pc.first.shape());
-              o_pack.descs.push_back(nary_desc(NARY_COPY, st, {sv}));
+              o_pack.descs.push_back(ndesc(NARY_COPY, st, {sv}));
               sp = st.ptr;
             }
             o_xchg.x.push_back(Xfer{rank_of(d), true, const_cast<float*>(sp), bytes, sn});
@@ -808,6 +819,7 @@ struct Lowerer {
 };
 
 void lower(PlanRt& P, bool dry) {
+  g_es = P.esize;
   P.main = Program{};
   P.carry = Program{};
   P.init = InitBatch{};
@@ -834,10 +846,19 @@ void lower(PlanRt& P, bool dry) {
 }
 
 void prepare_program(PlanRt& P, Program& prog) {
-  for (auto& b : prog.nary) nary_prepare(b);
-  for (auto& b : prog.conv) conv_prepare(b);
-  for (auto& specs : prog.gemm_specs)
+  const bool bf = P.esize == 2;
+  for (auto& b : prog.nary) {
+    b.bf16 = bf;
+    nary_prepare(b);
+  }
+  for (auto& b : prog.conv) {
+    b.bf16 = bf;
+    conv_prepare(b);
+  }
+  for (auto& specs : prog.gemm_specs) {
+    for (auto& sp : specs) sp.bf16 = bf;
     prog.gemm.push_back(gemm_prepare(specs, P.ctx->num_sms, P.precision == 1));
+  }
 }
 
 void free_program(Program& prog) {
@@ -866,10 +887,19 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
   P->flags = flags;
   P->stream = ctx->stream;
   if (precision != 0 && precision != 1) fail("unknown precision " + std::to_string(precision));
-  for (const auto& kv : P->plan.tensors)
-    if (kv.second.dtype_bytes != 4)
-      fail("tensor " + kv.first + " has dtype_bytes " + std::to_string(kv.second.dtype_bytes) +
-           "; this executor runs fp32 (dtype_bytes 4) plans");
+  // storage type = the graph's dtype: 4 -> fp32 (TF32 or 3xTF32 products), 2 -> bf16 (kind::f16
+  // products, fp32 accumulation); one type per plan
+  P->esize = 0;
+  for (const auto& kv : P->plan.tensors) {
+    const int db = kv.second.dtype_bytes;
+    if (db != 4 && db != 2)
+      fail("tensor " + kv.first + " has dtype_bytes " + std::to_string(db) +
+           "; this executor runs fp32 (4) and bf16 (2) plans");
+    if (P->esize && P->esize != db) fail("plan mixes dtype_bytes " + std::to_string(P->esize) + " and " + std::to_string(db));
+    P->esize = db;
+  }
+  if (!P->esize) P->esize = 4;
+  if (P->esize == 2 && precision == 1) fail("the 3xTF32 (fp32-accurate) mode needs an fp32 plan");
   const int devices = P->plan.devices;
   if (ctx->world > devices)
     fail("plan has " + std::to_string(devices) + " devices but the job has " + std::to_string(ctx->world) + " ranks");
@@ -895,6 +925,7 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
     lower(*P, false);
     prepare_program(*P, P->main);
     prepare_program(*P, P->carry);
+    P->init.bf16 = P->esize == 2;
     init_prepare(P->init);
   } else {
     P->arena_bytes = P->arena_used;
@@ -967,7 +998,7 @@ void init_inputs(PlanRt& P, uint64_t seed) {
 static void ensure_io(PlanRt& P, int64_t n) {
   if (P.io_tmp_elems >= size_t(n)) return;
   if (P.io_tmp) cudaFree(P.io_tmp);
-  CUDA_CHECK(cudaMalloc(&P.io_tmp, size_t(std::max<int64_t>(n, 1)) * 4));
+  CUDA_CHECK(cudaMalloc(&P.io_tmp, size_t(std::max<int64_t>(n, 1)) * 4));  // room for fp32 or bf16
   P.io_tmp_elems = size_t(n);
 }
 
@@ -982,48 +1013,79 @@ static const StridedView& node_val(PlanRt& P, int node, int64_t n) {
   return v;
 }
 
+// Raw storage-type I/O: n elements of the plan's storage type (fp32 or bf16) in host memory.
 void read_node_f32(PlanRt& P, int node, float* dst, int64_t n) {
+  g_es = P.esize;
   const StridedView& v = node_val(P, node, n);
   const float* src = v.ptr;
   if (!v.contiguous()) {
     ensure_io(P, n);
     NaryBatch b;
-    b.descs.push_back(nary_desc(NARY_COPY, contiguous_view(P.io_tmp, std::vector<int64_t>(v.shape, v.shape + v.rank)), {v}));
+    b.bf16 = P.esize == 2;
+    b.descs.push_back(ndesc(NARY_COPY, contiguous_view(P.io_tmp, std::vector<int64_t>(v.shape, v.shape + v.rank)), {v}));
     nary_prepare(b);
     nary_run(b, P.stream);
     CUDA_CHECK(cudaStreamSynchronize(P.stream));
     nary_free(b);
     src = P.io_tmp;
   }
-  CUDA_CHECK(cudaMemcpyAsync(dst, src, size_t(n) * 4, cudaMemcpyDeviceToHost, P.stream));
+  CUDA_CHECK(cudaMemcpyAsync(dst, src, size_t(n) * size_t(P.esize), cudaMemcpyDeviceToHost, P.stream));
   CUDA_CHECK(cudaStreamSynchronize(P.stream));
 }
 
 void write_node_f32(PlanRt& P, int node, const float* src, int64_t n) {
+  g_es = P.esize;
   const StridedView& v = node_val(P, node, n);
   if (v.contiguous()) {
-    CUDA_CHECK(cudaMemcpyAsync(v.ptr, src, size_t(n) * 4, cudaMemcpyHostToDevice, P.stream));
+    CUDA_CHECK(cudaMemcpyAsync(v.ptr, src, size_t(n) * size_t(P.esize), cudaMemcpyHostToDevice, P.stream));
     return;
   }
   ensure_io(P, n);
-  CUDA_CHECK(cudaMemcpyAsync(P.io_tmp, src, size_t(n) * 4, cudaMemcpyHostToDevice, P.stream));
+  CUDA_CHECK(cudaMemcpyAsync(P.io_tmp, src, size_t(n) * size_t(P.esize), cudaMemcpyHostToDevice, P.stream));
   NaryBatch b;
-  b.descs.push_back(nary_desc(NARY_COPY, v, {contiguous_view(P.io_tmp, std::vector<int64_t>(v.shape, v.shape + v.rank))}));
+  b.bf16 = P.esize == 2;
+  b.descs.push_back(ndesc(NARY_COPY, v, {contiguous_view(P.io_tmp, std::vector<int64_t>(v.shape, v.shape + v.rank))}));
   nary_prepare(b);
   nary_run(b, P.stream);
   CUDA_CHECK(cudaStreamSynchronize(P.stream));
   nary_free(b);
 }
 
+// bf16 <-> fp32 on the host: bf16 is the top half of an fp32; fp32 -> bf16 rounds to nearest
+// even (NaN kept quiet), matching __float2bfloat16_rn.
+static inline float bf16_to_f32(uint16_t h) {
+  const uint32_t u = uint32_t(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+static inline uint16_t f32_to_bf16(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu)) return uint16_t((u >> 16) | 0x40);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
 void read_node(PlanRt& P, int node, double* dst, int64_t n) {
   std::vector<float> tmp(size_t(std::max<int64_t>(n, 1)));
   read_node_f32(P, node, tmp.data(), n);
-  f32_to_f64_host(tmp.data(), dst, n);
+  if (P.esize == 2) {
+    const uint16_t* h = reinterpret_cast<const uint16_t*>(tmp.data());
+    for (int64_t i = 0; i < n; ++i) dst[i] = double(bf16_to_f32(h[i]));
+  } else {
+    f32_to_f64_host(tmp.data(), dst, n);
+  }
 }
 
 void write_node(PlanRt& P, int node, const double* src, int64_t n) {
   std::vector<float> tmp(size_t(std::max<int64_t>(n, 1)));
-  for (int64_t i = 0; i < n; ++i) tmp[size_t(i)] = float(src[i]);
+  if (P.esize == 2) {
+    uint16_t* h = reinterpret_cast<uint16_t*>(tmp.data());
+    for (int64_t i = 0; i < n; ++i) h[i] = f32_to_bf16(float(src[i]));
+  } else {
+    for (int64_t i = 0; i < n; ++i) tmp[size_t(i)] = float(src[i]);
+  }
   write_node_f32(P, node, tmp.data(), n);
   CUDA_CHECK(cudaStreamSynchronize(P.stream));
 }
@@ -1042,7 +1104,7 @@ std::string describe(const PlanRt& P) {
         const NaryBatch& b = prog.nary[size_t(st.idx)];
         s << ",\"descs\":" << b.descs.size();
         double bytes = 0;
-        for (const auto& d : b.descs) bytes += 4.0 * double(d.units) * d.vec * (d.nin + 1);
+        for (const auto& d : b.descs) bytes += double(P.esize) * double(d.units) * d.vec * (d.nin + 1);
         s << ",\"bytes\":" << int64_t(bytes);
       } else if (st.kind == ST_GEMM) {
         const auto& specs = prog.gemm_specs[size_t(st.idx)];

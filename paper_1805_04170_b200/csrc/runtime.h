@@ -72,6 +72,7 @@ struct PlanRt {
   Plan plan;
   int precision = 0;
   int flags = 0;
+  int esize = 4;                 // storage bytes per element: 4 fp32, 2 bf16 (the plan's dtype)
   std::vector<int> dev_rank;
   std::vector<StridedView> val;
   std::vector<char> has_val;

@@ -162,11 +162,16 @@ class PlanExecutor:
         check(lib().tpx_write_node(self._h, node_id.encode(),
                                    v.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), v.size))
 
+    # Raw storage I/O: n elements of the plan's storage type (fp32, or bf16 for dtype_bytes-2
+    # plans; see storage_bytes()) between host memory and a node's holder block.
     def read_node_f32_into(self, node_id: str, host_ptr: int, n: int):
         check(lib().tpx_read_node_f32(self._h, node_id.encode(), ctypes.c_void_p(host_ptr), n))
 
     def write_node_f32_from(self, node_id: str, host_ptr: int, n: int):
         check(lib().tpx_write_node_f32(self._h, node_id.encode(), ctypes.c_void_p(host_ptr), n))
+
+    def storage_bytes(self) -> int:
+        return int(self.stats()["storage_bytes"])
 
     def node_view(self, node_id: str):
         p, r = ctypes.c_uint64(), ctypes.c_int()

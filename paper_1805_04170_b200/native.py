@@ -29,6 +29,7 @@ class Stats(ctypes.Structure):
         ("n_steps", c_i64), ("n_kernel_launches", c_i64), ("n_gemm_launches", c_i64),
         ("n_copy_launches", c_i64), ("n_nccl_groups", c_i64), ("n_fused_ew", c_i64),
         ("device_bytes", c_i64), ("gemm_flops", c_dbl), ("gemm_min_bytes", c_dbl),
+        ("storage_bytes", c_i64),
     ]
 
     def as_dict(self):
