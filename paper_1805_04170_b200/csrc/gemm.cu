@@ -1146,6 +1146,9 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   g.swap = (M0 < 128 && N0 >= 2 * M0);
   const long long Q0 = g.swap ? M0 : N0;
   g.bn = Q0 <= 32 ? 32 : Q0 <= 64 ? 64 : Q0 <= 128 ? 128 : 256;
+  // an MN-major bf16 Q operand is staged in 64-element (128-byte) chunks: BN >= 64
+  const bool q_mn0 = g.swap ? s0.ta : !s0.tb;
+  if (s0.bf16 && q_mn0 && g.bn < 64) g.bn = 64;
   g.nprob = int(specs.size());
   // CTA pairs (256 x 256 tiles, half the operand bytes per SM) for wide TF32 problems
   const long long P0 = g.swap ? N0 : M0;

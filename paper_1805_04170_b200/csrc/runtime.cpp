@@ -232,8 +232,8 @@ struct Lowerer {
       StridedView b = value(n.sources[1]);
       s.a = mat_view(a);
       s.b = mat_view(b);
-      if (!gemm_view_ok(s.a)) s.a = mat_view(materialize(n.sources[0], op.id));
-      if (!gemm_view_ok(s.b)) s.b = mat_view(materialize(n.sources[1], op.id));
+      if (!gemm_view_ok(s.a, g_es == 2)) s.a = mat_view(materialize(n.sources[0], op.id));
+      if (!gemm_view_ok(s.b, g_es == 2)) s.b = mat_view(materialize(n.sources[1], op.id));
       s.ta = op.ta;
       s.tb = op.tb;
       s.c = out.ptr;
@@ -288,7 +288,7 @@ struct Lowerer {
     m.cols = k.shape[1] * k.shape[2] * k.shape[3];
     m.rs = k.st[0];
     m.cs = 1;
-    return gemm_view_ok(m);
+    return gemm_view_ok(m, g_es == 2);
   }
   // 16-byte rows (TMA): 4 fp32 or 8 bf16 elements
   static int64_t pitch4(int64_t n) { const int64_t a = 16 / g_es; return (n + a - 1) / a * a; }
@@ -427,7 +427,8 @@ struct Lowerer {
       const int64_t C = b.shape[1], U = b.shape[2], V = b.shape[3], K = C * U * V, YX = Yo * Xo;
       const MatView km = filter(b);
       StridedView g = a;
-      if (!(g.st[3] == 1 && g.st[2] == Xo && g.st[1] % 4 == 0 && g.st[0] % 4 == 0 &&
+      const int64_t al = 16 / g_es;  // elements per 16 bytes
+      if (!(g.st[3] == 1 && g.st[2] == Xo && g.st[1] % al == 0 && g.st[0] % al == 0 &&
             (reinterpret_cast<uintptr_t>(g.ptr) & 15) == 0))
         g = padded_copy(a, 2, op.id);
       const int64_t img = pitch4(YX), ld = pitch4(NB * img);

@@ -8,6 +8,11 @@ tests/test_oracle.py) supplies every node's fp64 value.  Two checks per plan (SU
   (normwise max|d| / max|ref| per block):
       PREC_FP32 (3xTF32 split, fp32-accurate products)   <= 1e-5
       PREC_TF32 (single-pass kind::tf32, fp32 accumulate) <= 2e-3
+* bf16 plans (graph dtype_bytes 2, "_bf16" stems): bf16 storage, kind::f16 products with
+  fp32 accumulation, every stored value rounded to bf16.  Per-op teacher-forced gate
+  <= 1e-2 normwise: the oracle's inputs are rounded to bf16 when written and the output is
+  rounded again, and values reach |1| where the bf16 spacing is 2^-7 (two roundings <= 0.6 %
+  of max|ref|).  Chained values are checked finite and reported, not gated.
 * chained: the whole step from seeded inputs.  The reference's op semantics make the
   backward chain ill-conditioned (dact = 1 - tanh^2(h) on unscaled U[-1,1) inits), so the
   chained gate applies to the fp32-accurate path only: <= 5e-2 normwise on every holder;
@@ -26,7 +31,12 @@ pytestmark = pytest.mark.gpu
 
 STEMS = golden_stems()
 TOL_OP = {1: 1e-5, 0: 2e-3}
+TOL_OP_BF16 = 1e-2
 TOL_CHAIN_FP32 = 5e-2
+
+
+def is_bf16(stem):
+    return "_bf16" in stem
 
 
 @pytest.fixture(scope="module")
@@ -88,18 +98,25 @@ def run_chained(ctx, stem, precision, flags=1):
 
 @pytest.mark.parametrize("stem", STEMS, ids=stem_id)
 def test_per_op_fp32(ctx, stem):
+    if is_bf16(stem):
+        pytest.skip("3xTF32 is an fp32-storage mode")
     e, op = run_per_op(ctx, stem, 1)
     assert e <= TOL_OP[1], (op, e)
 
 
 @pytest.mark.parametrize("stem", STEMS, ids=stem_id)
 def test_per_op_tf32(ctx, stem):
+    """TF32 products on fp32 plans; bf16 products and storage on bf16 plans."""
     e, op = run_per_op(ctx, stem, 0)
-    assert e <= TOL_OP[0], (op, e)
+    assert e <= (TOL_OP_BF16 if is_bf16(stem) else TOL_OP[0]), (op, e)
 
 
 @pytest.mark.parametrize("stem", STEMS, ids=stem_id)
 def test_chained_fp32(ctx, stem):
+    if is_bf16(stem):
+        e, t = run_chained(ctx, stem, 0)
+        assert np.isfinite(e), (t, e)  # bf16 chained error: reported, not gated (SURVEY §7 H5)
+        return
     e, t = run_chained(ctx, stem, 1)
     assert e <= TOL_CHAIN_FP32, (t, e)
 
@@ -110,8 +127,9 @@ def test_chained_forced_exchange(ctx, stem):
     one GPU): identical results to the HBM-copy lowering."""
     from paper_1805_04170_b200.executor import PlanExecutor
     text, P, seed, _, _ = oracle_values(stem)
-    a = PlanExecutor(ctx, text, precision=1, flags=1)
-    b = PlanExecutor(ctx, text, precision=1, flags=3)
+    prec = 0 if is_bf16(stem) else 1
+    a = PlanExecutor(ctx, text, precision=prec, flags=1)
+    b = PlanExecutor(ctx, text, precision=prec, flags=3)
     for ex in (a, b):
         ex.init_inputs(seed)
         ex.execute()
@@ -127,8 +145,9 @@ def test_unfused_matches_fused(ctx, stem):
     whether it runs in the GEMM epilogue or as its own launch."""
     from paper_1805_04170_b200.executor import PlanExecutor
     text, P, seed, _, _ = oracle_values(stem)
-    a = PlanExecutor(ctx, text, precision=1, flags=1)
-    b = PlanExecutor(ctx, text, precision=1, flags=0)
+    prec = 0 if is_bf16(stem) else 1
+    a = PlanExecutor(ctx, text, precision=prec, flags=1)
+    b = PlanExecutor(ctx, text, precision=prec, flags=0)
     assert a.stats()["n_fused_ew"] > 0 and b.stats()["n_fused_ew"] == 0
     for ex in (a, b):
         ex.init_inputs(seed)
@@ -230,3 +249,35 @@ def test_tensor_core_conv_matches_direct(ctx, stem):
             assert normwise(outs[0][h], outs[1][h]) <= 1e-5, (op["id"], h)
     tc.close()
     dc.close()
+
+
+def _bf16_round(x):
+    """fp64 -> fp32 (nearest) -> bf16 (nearest even), as fp64."""
+    f = np.asarray(x, dtype=np.float64).astype(np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16 << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def test_seeded_inputs_bit_exact_bf16(ctx):
+    """bf16 plans: every input block holds seeded_tensor's fp64 value rounded to fp32 then to
+    bf16 (round to nearest even)."""
+    from paper_1805_04170_b200.executor import PlanExecutor
+    stem = [s for s in STEMS if "cfg1_bf16.opt.k1" in s][0]
+    text, P, seed, serial, vals = oracle_values(stem)
+    ex = PlanExecutor(ctx, text)
+    assert ex.storage_bytes() == 2
+    ex.init_inputs(seed)
+    ex.synchronize()
+    for n in P["nodes"]:
+        if n["kind"] == "buffer":
+            assert np.array_equal(ex.read_node(n["id"]), _bf16_round(vals[n["id"]])), n["id"]
+
+
+def test_bf16_fp32_same_plan_structure(ctx):
+    """A bf16 plan is the fp32 plan with halved bytes: same nodes, regions and tilings."""
+    import gzip
+    a = json.loads(gzip.open([s for s in STEMS if "cfg1_bf16.opt.k1" in s][0] + ".plan.json.gz", "rt").read())
+    b = json.loads(gzip.open([s for s in STEMS if "cfg1_mlp3x1024_b64.opt.k1" in s][0] + ".plan.json.gz", "rt").read())
+    assert [(n["id"], n["region"]) for n in a["nodes"]] == [(n["id"], n["region"]) for n in b["nodes"]]
+    assert a["fetch_bytes_total"] * 2 == b["fetch_bytes_total"]

@@ -69,6 +69,13 @@ def graphs() -> dict:
     g["cnnr_train_b16"] = ref.gen_cnn(16, (10, 10), [4, 8, 8], (3, 3), backward=True)
     # AlexNet-style conv component (per-layer filters + SGD update; paper_1805_04170_b200/graphs.py)
     g["alexr_conv_b4"] = G.conv_net(4, (16, 16), [3, 8, 16, 8], [(5, 5), (3, 3), (3, 3)])
+    # bf16 storage (dtype_bytes 2): same structures, the planner's bytes halve; the reference's
+    # fp64 values are dtype-independent
+    g["cfg1_bf16"] = ref.gen_mlp(64, [1024] * 4, dtype_bytes=2)
+    g["cfg2r_bf16"] = ref.gen_mlp(64, [256] * 6, dtype_bytes=2)
+    g["mlp_train_d2_bf16"] = ref.gen_mlp(8, [8] * 3, dtype_bytes=2)
+    g["fcr_alexnet_bf16"] = ref.gen_mlp(32, [576, 256, 256, 64], dtype_bytes=2)
+    g["alexr_conv_bf16"] = G.conv_net(4, (16, 16), [3, 8, 16, 8], [(5, 5), (3, 3), (3, 3)], dtype_bytes=2)
     g["reduce_kat"] = reduce_kat_graph()
     return g
 
@@ -102,6 +109,11 @@ def cases():
     for k in (1, 2):
         out.append(("alexr_conv_b4", "data", k, 7))
     out.append(("alexr_conv_b4", "model", 2, 7))
+    for name, ks in (("cfg1_bf16", (0, 1)), ("cfg2r_bf16", (0, 2)), ("mlp_train_d2_bf16", (1, 2)),
+                     ("fcr_alexnet_bf16", (1,)), ("alexr_conv_bf16", (0, 1))):
+        for k in ks:
+            out.append((name, "opt", k, 7))
+        out.append((name, "data", max(ks[-1], 1), 7))
     out.append(("reduce_kat", "custom", 1, 5))
     return out
 
