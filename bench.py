@@ -277,7 +277,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2_mlp5x8192_b512", choices=sorted(CONFIGS) + sorted(NETWORKS))
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32", "bf16"])
+    ap.add_argument("--no-variants", action="store_true", help="skip the bf16 variant beside a tf32 run")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -314,17 +315,18 @@ def main():
 
     parts = parts_of(args.config)
     batch = workload_batch(args.config)
-    prec = 0 if args.precision == "tf32" else 1
+    prec = 1 if args.precision == "fp32" else 0  # bf16: storage type comes from the bf16 plan
     ctx = Context(local, rank, world)
     if world > 1:
         ctx.init_comm_from_torch()
     stream = torch.cuda.Stream()
     hbm_peak, bf16_peak, peak_kind = peaks()
     res = {}
-    for mode in ("opt", "data"):
+    def measure(mode, suffix, prec):
+        """One plan set (every component of the workload) timed end to end."""
         exs, texts = [], []
         for part in parts:
-            text = load_plan(part, mode, k)
+            text = load_plan(part + suffix, mode, k)
             ex = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE)
             ex.set_stream(stream.cuda_stream)
             ex.init_inputs(SEED)
@@ -378,17 +380,18 @@ def main():
             roles = {t["id"]: t["role"] for t in plan["graph"]["tensors"]}
             src = [t for t, rl in roles.items() if rl == "input"]
             last = next(o["inputs"][0] for o in plan["graph"]["ops"] if o["id"] == "seed")
+            hdt = torch.bfloat16 if ex.storage_bytes() == 2 else torch.float32  # raw storage I/O
             for t in src:
                 for h in plan["holders"][t]:
                     if nodes[h]["device"] in mine:
-                        hin.append((ex, h, torch.empty(math.prod(ex.node_shape(h)), dtype=torch.float32,
+                        hin.append((ex, h, torch.empty(math.prod(ex.node_shape(h)), dtype=hdt,
                                                        pin_memory=True).uniform_(-1, 1)))
             for h in plan["holders"][last]:
                 if nodes[h]["device"] in mine:
-                    hout.append((ex, h, torch.empty(math.prod(ex.node_shape(h)), dtype=torch.float32,
+                    hout.append((ex, h, torch.empty(math.prod(ex.node_shape(h)), dtype=hdt,
                                                     pin_memory=True)))
-        h2d = sum(v.numel() * 4 for _, _, v in hin)
-        d2h = sum(v.numel() * 4 for _, _, v in hout)
+        h2d = sum(v.numel() * v.element_size() for _, _, v in hin)
+        d2h = sum(v.numel() * v.element_size() for _, _, v in hout)
 
         def e2e_step():
             for ex, h, v in hin:
@@ -406,9 +409,23 @@ def main():
             dist.all_reduce(tot)
         r["e2e"] = {"value": batch * args.steps / (e_ms / 1e3), "unit": "samples/s",
                     "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item())}
-        res[mode] = r
         for ex in exs:
             ex.close()
+        return r
+
+    suffix = "_bf16" if args.precision == "bf16" else ""
+    for mode in ("opt", "data"):
+        res[mode] = measure(mode, suffix, prec)
+    # the bf16-storage variant of the optimal plan, reported beside the TF32 headline
+    variants = {}
+    if args.precision == "tf32" and not args.no_variants:
+        try:
+            vb = measure("opt", "_bf16", 0)
+            variants["bf16"] = {"value": vb["value"], "ms_per_step": vb["ms_per_step"], "e2e": vb["e2e"],
+                                "dtype": "bf16", "plan": f"kcuts optimal k={k}, graph dtype_bytes 2",
+                                "gemm_ms_per_step": vb["gemm_ms"]}
+        except FileNotFoundError:
+            pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -431,14 +448,15 @@ def main():
     o, d = res["opt"], res["data"]
     flops = o["stats"]["gemm_flops"]
     tf32_peak = bf16_peak / 2
-    peak = tf32_peak if prec == 0 else tf32_peak / 3
+    peak = bf16_peak if args.precision == "bf16" else tf32_peak if prec == 0 else tf32_peak / 3
     kernels, dom = kernel_rooflines(o, peak, hbm_peak)
     traffic = (measured_traffic().get(dom["class"]) or {}).get("dram_bytes_per_launch") if dom else None
     line = {
         "metric": METRIC, "value": o["value"], "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": o["ms_per_step"],
         "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "tf32" if prec == 0 else "fp32(3xtf32)", "data": "synthetic",
+        "vs_baseline": None, "dtype": {"tf32": "tf32", "fp32": "fp32(3xtf32)", "bf16": "bf16"}[args.precision],
+        "data": "synthetic",
         "config": workload_config(args.config, k),
         "dp": {"value": d["value"], "ms_per_step": d["ms_per_step"], "plan": f"preset data k={k}",
                "e2e": d["e2e"]["value"], "fetch_bytes_total": d["stats"]["fetch_bytes_total"]},
@@ -452,7 +470,8 @@ def main():
                      "algorithmic_per_launch": dom["per_launch"], "avg_launch_ms": dom["ms"],
                      "share_of_step": dom["share"],
                      "peak_basis": (f"{peak_kind} MEASURED_PEAKS: HBM {hbm_peak} GB/s; tensor = bf16 {bf16_peak} "
-                                    f"TFLOP/s / 2 (kind::tf32 issues at half the kind::f16 rate)"
+                                    f"TFLOP/s" + ("" if args.precision == "bf16" else
+                                                  " / 2 (kind::tf32 issues at half the kind::f16 rate)")
                                     + (" / 3 (3xTF32 split)" if prec else "")),
                      "kernels": kernels,
                      "flops_per_step": flops, "gemm_ms_per_step": o["gemm_ms"],
@@ -461,6 +480,7 @@ def main():
                      "step_frac": step_roofline_ms(kernels) / o["ms_per_step"]},
         "clocks": o["clocks"],
         "cpu_baseline": cpu,
+        "variants": variants,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -60,17 +60,32 @@ def write(path, text):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
-    names = sys.argv[1:] or list(CONFIGS) + list(CONV_CONFIGS)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    bf16 = "--bf16" in sys.argv  # dtype_bytes 2 variants: plans/<name>_bf16.<mode>.k<k>
+    names = args or list(CONFIGS) + list(CONV_CONFIGS)
     for name in names:
-        g = CONV_CONFIGS[name]() if name in CONV_CONFIGS else ref.gen_mlp(*CONFIGS[name])
+        db = 2 if bf16 else 4
+        if name in CONV_CONFIGS:
+            g = CONV_CONFIGS[name]()
+            if bf16:
+                gj = json.loads(g)
+                for t in gj["tensors"]:
+                    t["dtype_bytes"] = 2
+                g = json.dumps(gj, sort_keys=True)
+        else:
+            batch, dims = CONFIGS[name]
+            g = ref.gen_mlp(batch, dims, dtype_bytes=db)
+        out_name = name + ("_bf16" if bf16 else "")
         for mode in ("opt", "data"):
             for k in range(4):
                 text = ref.plan(g, mode, k)
                 P = json.loads(text)
-                path = os.path.join(OUT, f"{name}.{mode}.k{k}.plan.json.gz")
+                path = os.path.join(OUT, f"{out_name}.{mode}.k{k}.plan.json.gz")
                 write(path, text)
                 print(f"{os.path.basename(path)}: {len(P['nodes'])} nodes, "
                       f"fetch_bytes_total {P['fetch_bytes_total']}")
+        if bf16:
+            continue
         if name in CONV_SAMPLES:
             sname, gen = CONV_SAMPLES[name]
             write(os.path.join(OUT, f"{sname}.opt.k0.plan.json.gz"), ref.plan(gen(), "opt", 0))
