@@ -106,8 +106,9 @@ def main():
         # --one M N K ta tb [epi,...]: one timed configuration (for ncu)
         i = sys.argv.index("--one")
         M, N, K, ta, tb = (int(x) for x in sys.argv[i + 1:i + 6])
-        epi = [int(x) for x in sys.argv[i + 6].split(",")] if len(sys.argv) > i + 6 else None
-        ms, tf, gb = bench(M, N, K, bool(ta), bool(tb), iters=3, epi=epi)
+        epi = [int(x) for x in sys.argv[i + 6].split(",")] if len(sys.argv) > i + 6 and sys.argv[i + 6] != "-" else None
+        prec = int(sys.argv[i + 7]) if len(sys.argv) > i + 7 else 0
+        ms, tf, gb = bench(M, N, K, bool(ta), bool(tb), iters=3, epi=epi, precision=prec)
         print(f"one {(M, N, K, ta, tb)} epi={epi}: {ms:.3f} ms {tf:.1f} TFLOP/s {gb:.0f} GB/s")
         return
     cases = [
