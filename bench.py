@@ -279,6 +279,7 @@ def main():
     ap.add_argument("--config", default="cfg2_mlp5x8192_b512", choices=sorted(CONFIGS) + sorted(NETWORKS))
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32", "bf16"])
     ap.add_argument("--no-variants", action="store_true", help="skip the bf16 variant beside a tf32 run")
+    ap.add_argument("--no-graph", action="store_true", help="launch the lowered steps one by one")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -288,7 +289,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_1805_04170_b200.executor import FLAG_FUSE, Context, PlanExecutor
+    from paper_1805_04170_b200.executor import FLAG_FUSE, FLAG_GRAPH, Context, PlanExecutor
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -327,7 +328,7 @@ def main():
         exs, texts = [], []
         for part in parts:
             text = load_plan(part + suffix, mode, k)
-            ex = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE)
+            ex = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE | (0 if args.no_graph else FLAG_GRAPH))
             ex.set_stream(stream.cuda_stream)
             ex.init_inputs(SEED)
             exs.append(ex)

@@ -82,6 +82,8 @@ typedef struct tpx_plan tpx_plan;
 #define TPX_FLAG_FORCE_XCHG 2
 /* Convolutions on CUDA cores (direct loops) instead of im2col + tcgen05 GEMM (cross-check). */
 #define TPX_FLAG_DIRECT_CONV 4
+/* Execute the step as one CUDA graph (captured on the first tpx_execute on a stream). */
+#define TPX_FLAG_GRAPH 8
 int tpx_load_plan(tpx_ctx* ctx, const char* plan_json, size_t len, int precision, int flags,
                   tpx_plan** out);
 int tpx_plan_free(tpx_plan* plan);

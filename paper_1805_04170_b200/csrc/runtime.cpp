@@ -872,6 +872,7 @@ void free_program(Program& prog) {
 }  // namespace
 
 PlanRt::~PlanRt() {
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
   free_program(main);
   free_program(carry);
   init_free(init);
@@ -955,6 +956,29 @@ static void launch_step(PlanRt& P, Program& prog, const Step& s, cudaStream_t st
 void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
   if (P.ctx->host_only()) fail("host-only context cannot execute plans");
   cudaStream_t st = P.stream;
+  if ((P.flags & 8) && !P.timing && !only_op && &prog == &P.main) {
+    // CUDA graph of the whole lowered step (captured on first use, replayed after; the
+    // stream must not change in between): one launch instead of one per lowered step
+    if (!P.graph_exec || P.graph_stream != st) {
+      if (P.graph_exec) cudaGraphExecDestroy(P.graph_exec);
+      P.graph_exec = nullptr;
+      cudaGraph_t g = nullptr;
+      CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        for (const auto& s : prog.steps) launch_step(P, prog, s, st);
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      CUDA_CHECK(cudaStreamEndCapture(st, &g));
+      CUDA_CHECK(cudaGraphInstantiate(&P.graph_exec, g, 0));
+      cudaGraphDestroy(g);
+      P.graph_stream = st;
+    }
+    CUDA_CHECK(cudaGraphLaunch(P.graph_exec, st));
+    return;
+  }
   if (!P.timing || only_op) {
     for (const auto& s : prog.steps)
       if (!only_op || s.op == *only_op) launch_step(P, prog, s, st);

@@ -97,6 +97,9 @@ struct PlanRt {
   float* io_tmp = nullptr;
   size_t io_tmp_elems = 0;
   cudaStream_t stream = nullptr;
+  // TPX_FLAG_GRAPH: the main program captured as one CUDA graph
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t graph_stream = nullptr;
 
   ~PlanRt();
   bool mine(int node) const { return dev_rank[size_t(plan.nodes[size_t(node)].device)] == ctx->rank; }

@@ -29,6 +29,7 @@ PREC_FP32 = 1
 FLAG_FUSE = 1
 FLAG_FORCE_XCHG = 2
 FLAG_DIRECT_CONV = 4  # convolutions as direct CUDA-core loops (cross-check of the tcgen05 lowering)
+FLAG_GRAPH = 8        # the whole step replayed as one CUDA graph
 
 
 @dataclass

@@ -281,3 +281,40 @@ def test_bf16_fp32_same_plan_structure(ctx):
     b = json.loads(gzip.open([s for s in STEMS if "cfg1_mlp3x1024_b64.opt.k1" in s][0] + ".plan.json.gz", "rt").read())
     assert [(n["id"], n["region"]) for n in a["nodes"]] == [(n["id"], n["region"]) for n in b["nodes"]]
     assert a["fetch_bytes_total"] * 2 == b["fetch_bytes_total"]
+
+
+@pytest.mark.parametrize("stem", [s for s in STEMS if ".k2." in s and ("cfg2r" in s or "alexr_conv" in s or "mlp_train_d3" in s)][:6],
+                         ids=stem_id)
+def test_graph_replay_matches(ctx, stem):
+    """TPX_FLAG_GRAPH (the step captured once as a CUDA graph and replayed) changes no bits."""
+    from paper_1805_04170_b200.executor import FLAG_FUSE, FLAG_GRAPH, PlanExecutor
+    text, P, seed, _, _ = oracle_values(stem)
+    prec = 0 if is_bf16(stem) else 1
+    a = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE)
+    b = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE | FLAG_GRAPH)
+    for ex in (a, b):
+        ex.init_inputs(seed)
+        for _ in range(2):  # capture, then replay
+            ex.execute()
+        ex.synchronize()
+    for hs in P["holders"].values():
+        for hid in hs:
+            assert np.array_equal(a.read_node(hid), b.read_node(hid)), hid
+
+
+def test_graph_replay_with_nccl_exchange(ctx):
+    """The captured graph also holds the NCCL send/recv groups (forced exchange, self-peer)."""
+    from paper_1805_04170_b200.executor import FLAG_FORCE_XCHG, FLAG_FUSE, FLAG_GRAPH, PlanExecutor
+    stem = [s for s in STEMS if "cfg2r_mlp5x256_b64.opt.k2" in s][0]
+    text, P, seed, _, _ = oracle_values(stem)
+    a = PlanExecutor(ctx, text, precision=1, flags=FLAG_FUSE | FLAG_FORCE_XCHG)
+    b = PlanExecutor(ctx, text, precision=1, flags=FLAG_FUSE | FLAG_FORCE_XCHG | FLAG_GRAPH)
+    assert b.stats()["n_nccl_groups"] > 0
+    for ex in (a, b):
+        ex.init_inputs(seed)
+        for _ in range(2):
+            ex.execute()
+        ex.synchronize()
+    for hs in P["holders"].values():
+        for hid in hs:
+            assert np.array_equal(a.read_node(hid), b.read_node(hid)), hid
