@@ -124,6 +124,13 @@ int tpx_synchronize(tpx_plan* plan);
 /* Per-step device timing of the last tpx_execute (events around each step): total ms and
  * ms spent in GEMM launches. */
 int tpx_last_timing(const tpx_plan* plan, double* total_ms, double* gemm_ms, double* copy_ms);
+/* Steps [begin, end) of the lowered step program (the order of tpx_plan_describe()'s "main"
+ * steps), on the plan stream; with TPX_FLAG_GRAPH each range is captured once as a CUDA graph.
+ * Lets a caller overlap its own copies (next batch in, network output out) with the step. */
+int tpx_execute_steps(tpx_plan* plan, int64_t begin, int64_t end);
+/* Device-to-device copy between a node's holder block and n contiguous elements of the storage
+ * type at `dev` (to_node != 0: into the node), on the plan stream. */
+int tpx_copy_node_device(tpx_plan* plan, const char* node_id, void* dev, int64_t n, int to_node);
 /* Per-step device times (ms) of the last timed execution, in the order of
  * tpx_plan_describe()'s "main" steps; fills min(n, *n_steps) entries. */
 int tpx_last_step_times(const tpx_plan* plan, double* ms, int64_t n, int64_t* n_steps);

@@ -188,6 +188,17 @@ TPX_API int tpx_execute(tpx_plan* plan) {
   return tpx::guard([&] { tpx::run_program(rt(plan), rt(plan).main, nullptr); });
 }
 
+TPX_API int tpx_execute_steps(tpx_plan* plan, int64_t begin, int64_t end) {
+  return tpx::guard([&] { tpx::run_steps(rt(plan), begin, end); });
+}
+
+TPX_API int tpx_copy_node_device(tpx_plan* plan, const char* node_id, void* dev, int64_t n, int to_node) {
+  return tpx::guard([&] {
+    tpx::PlanRt& P = rt(plan);
+    tpx::copy_node_device(P, node_of(P, node_id), dev, n, to_node != 0);
+  });
+}
+
 TPX_API int tpx_execute_op(tpx_plan* plan, const char* op_id) {
   return tpx::guard([&] {
     tpx::PlanRt& P = rt(plan);

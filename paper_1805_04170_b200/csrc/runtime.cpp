@@ -873,6 +873,7 @@ void free_program(Program& prog) {
 
 PlanRt::~PlanRt() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  for (auto& kv : range_graphs) cudaGraphExecDestroy(kv.second);
   free_program(main);
   free_program(carry);
   init_free(init);
@@ -1006,6 +1007,63 @@ void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
     if (prog.steps[i].kind == ST_GEMM) P.last_gemm_ms += ms;
     else if (prog.steps[i].kind == ST_NARY || prog.steps[i].kind == ST_XCHG) P.last_copy_ms += ms;
   }
+}
+
+static const StridedView& node_val(PlanRt& P, int node, int64_t n);
+
+void run_steps(PlanRt& P, int64_t begin, int64_t end) {
+  if (P.ctx->host_only()) fail("host-only context cannot execute plans");
+  Program& prog = P.main;
+  const int64_t n = int64_t(prog.steps.size());
+  if (begin < 0 || end > n || begin > end) fail("step range [" + std::to_string(begin) + ", " + std::to_string(end) +
+                                               ") outside the program's " + std::to_string(n) + " steps");
+  cudaStream_t st = P.stream;
+  if (P.flags & 8) {
+    auto key = std::make_pair(begin, end);
+    auto it = P.range_graphs.find(key);
+    if (it == P.range_graphs.end() || P.graph_stream != st) {
+      if (P.graph_stream != st) {
+        for (auto& kv : P.range_graphs) cudaGraphExecDestroy(kv.second);
+        P.range_graphs.clear();
+      }
+      cudaGraph_t g = nullptr;
+      CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        for (int64_t i = begin; i < end; ++i) launch_step(P, prog, prog.steps[size_t(i)], st);
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      CUDA_CHECK(cudaStreamEndCapture(st, &g));
+      cudaGraphExec_t ge = nullptr;
+      CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      P.graph_stream = st;
+      it = P.range_graphs.emplace(key, ge).first;
+    }
+    CUDA_CHECK(cudaGraphLaunch(it->second, st));
+    return;
+  }
+  for (int64_t i = begin; i < end; ++i) launch_step(P, prog, prog.steps[size_t(i)], st);
+}
+
+void copy_node_device(PlanRt& P, int node, void* dev, int64_t n, bool to_node) {
+  g_es = P.esize;
+  const StridedView& v = node_val(P, node, n);
+  if (v.contiguous()) {
+    if (to_node) CUDA_CHECK(cudaMemcpyAsync(v.ptr, dev, size_t(n) * size_t(P.esize), cudaMemcpyDeviceToDevice, P.stream));
+    else CUDA_CHECK(cudaMemcpyAsync(dev, v.ptr, size_t(n) * size_t(P.esize), cudaMemcpyDeviceToDevice, P.stream));
+    return;
+  }
+  NaryBatch b;
+  b.bf16 = P.esize == 2;
+  const StridedView flat = contiguous_view(static_cast<float*>(dev), std::vector<int64_t>(v.shape, v.shape + v.rank));
+  b.descs.push_back(to_node ? ndesc(NARY_COPY, v, {flat}) : ndesc(NARY_COPY, flat, {v}));
+  nary_prepare(b);
+  nary_run(b, P.stream);
+  CUDA_CHECK(cudaStreamSynchronize(P.stream));
+  nary_free(b);
 }
 
 void init_inputs(PlanRt& P, uint64_t seed) {

@@ -100,6 +100,7 @@ struct PlanRt {
   // TPX_FLAG_GRAPH: the main program captured as one CUDA graph
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t graph_stream = nullptr;
+  std::map<std::pair<int64_t, int64_t>, cudaGraphExec_t> range_graphs;  // run_steps ranges
 
   ~PlanRt();
   bool mine(int node) const { return dev_rank[size_t(plan.nodes[size_t(node)].device)] == ctx->rank; }
@@ -107,6 +108,11 @@ struct PlanRt {
 
 PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags);
 void run_program(PlanRt& p, Program& prog, const std::string* only_op);
+// Steps [begin, end) of the main program (CUDA graph per range with TPX_FLAG_GRAPH).
+void run_steps(PlanRt& p, int64_t begin, int64_t end);
+// Device-to-device copy between a node's holder block and contiguous device memory (n
+// elements of the storage type), on the plan stream.
+void copy_node_device(PlanRt& p, int node, void* dev, int64_t n, bool to_node);
 void init_inputs(PlanRt& p, uint64_t seed);
 void read_node(PlanRt& p, int node, double* dst, int64_t n);
 void write_node(PlanRt& p, int node, const double* src, int64_t n);

@@ -171,6 +171,14 @@ class PlanExecutor:
     def write_node_f32_from(self, node_id: str, host_ptr: int, n: int):
         check(lib().tpx_write_node_f32(self._h, node_id.encode(), ctypes.c_void_p(host_ptr), n))
 
+    def execute_steps(self, begin: int, end: int):
+        """Lowered steps [begin, end) (describe()['main']['steps'] order) on the plan stream."""
+        check(lib().tpx_execute_steps(self._h, int(begin), int(end)))
+
+    def copy_node_device(self, node_id: str, dev_ptr: int, n: int, to_node: bool):
+        """Device-to-device copy between a node and n contiguous storage elements at dev_ptr."""
+        check(lib().tpx_copy_node_device(self._h, node_id.encode(), ctypes.c_void_p(dev_ptr), n, int(to_node)))
+
     def storage_bytes(self) -> int:
         return int(self.stats()["storage_bytes"])
 

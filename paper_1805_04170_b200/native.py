@@ -62,6 +62,8 @@ _SIGS = {
     "tpx_last_timing": [c_vp, P(c_dbl), P(c_dbl), P(c_dbl)],
     "tpx_enable_timing": [c_vp, c_int],
     "tpx_last_step_times": [c_vp, P(c_dbl), c_i64, P(c_i64)],
+    "tpx_execute_steps": [c_vp, c_i64, c_i64],
+    "tpx_copy_node_device": [c_vp, c_char_p, c_vp, c_i64, c_int],
     "tpx_gemm": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_i64,
                  c_int, P(c_int), P(ctypes.c_float), P(c_vp), P(c_i64), P(c_vp), P(c_i64), c_int,
                  c_u64],
