@@ -920,6 +920,7 @@ bool g_no_stream = false;  // disable evict-first stores / operand policies
 const CUtensorMapL2promotion kOtherPromo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
                                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
 bool g_no_pair = false;
+int g_max_bn = 0;  // debug: cap the tile width
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1012,8 +1013,9 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 6) g_no_pair = (sbo == 1);  // (6,1) single-CTA tiles only
   if (lbo == 7) g_other_promo = sbo > 0 ? int(sbo) - 1 : 0;  // (7,n) operand promotion n-1
   if (lbo == 8) g_no_stream = (sbo == 1);  // (8,1) no L2 streaming hints
+  if (lbo == 9) g_max_bn = int(sbo);       // (9,n) tile width <= n
   if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
-  if (lbo >= 1 && lbo <= 8) g_dbg_lbo = g_dbg_sbo = 0;
+  if (lbo >= 1 && lbo <= 9) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1148,7 +1150,36 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   g.bn = Q0 <= 32 ? 32 : Q0 <= 64 ? 64 : Q0 <= 128 ? 128 : 256;
   // an MN-major bf16 Q operand is staged in 64-element (128-byte) chunks: BN >= 64
   const bool q_mn0 = g.swap ? s0.ta : !s0.tb;
-  if (s0.bf16 && q_mn0 && g.bn < 64) g.bn = 64;
+  const int min_bn = (s0.bf16 && q_mn0) ? 64 : 32;
+  g.bn = std::max(g.bn, min_bn);
+  {
+    // Tile width from the tile count: the widest tile that still gives every SM work.  Short-K
+    // (epilogue-bound) problems want a tile per CTA; long-K ones are balanced by stream-K and
+    // keep wide tiles while each tile is cut into at most ~5 k-ranges.
+    long long kmax = 0;
+    for (const auto& s : specs) kmax = std::max<long long>(kmax, s.ta ? s.a.rows : s.a.cols);
+    const long long kb = (kmax + (s0.bf16 ? 63 : 31)) / (s0.bf16 ? 64 : 32);
+    auto tiles = [&](int bn) {
+      const bool pair = !split && !g_no_pair && bn == 256 && (g.swap ? N0 : M0) >= 256 && num_sms >= 4;
+      const long long pbm = pair ? 256 : 128;
+      long long t = 0;
+      for (const auto& s : specs) {
+        const long long M = s.ta ? s.a.cols : s.a.rows, N = s.tb ? s.b.rows : s.b.cols;
+        const long long P = g.swap ? N : M, Q = g.swap ? M : N;
+        t += ((P + pbm - 1) / pbm) * ((Q + bn - 1) / bn);
+      }
+      return std::make_pair(t, pair ? num_sms / 2 : num_sms);
+    };
+    int pick = g.bn;
+    for (int bn = g.bn; bn >= min_bn; bn /= 2) {
+      pick = bn;
+      const auto tu = tiles(bn);
+      const long long need = kb <= 16 ? tu.second : std::max(1, tu.second / 5);
+      if (tu.first >= need) break;
+    }
+    g.bn = pick;
+  }
+  if (g_max_bn > 0) g.bn = std::max(min_bn, std::min(g.bn, g_max_bn));
   g.nprob = int(specs.size());
   // CTA pairs (256 x 256 tiles, half the operand bytes per SM) for wide TF32 problems
   const long long P0 = g.swap ? N0 : M0;
