@@ -291,7 +291,27 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restri
 
 // im2col / col2im of the tensor-core conv lowering: one warp per output row (lanes over x), so
 // reads and writes are coalesced and the index decomposition is paid once per row.
-constexpr int kRowsPerWarp = 8;
+constexpr int kRowsPerWarp = 32;     // im2col rows per warp (incremental row indices)
+constexpr int kColRowsPerWarp = 2;   // col2im output rows per warp (U*V taps each)
+constexpr int kColRowsPerBlock = (kThreads / 32) * kColRowsPerWarp;
+
+// Sum of the valid taps of a UxV filter for one col2im output element, fixed trip counts and
+// predicated loads, in (u, v) order (the direct conv's order).
+template <int UU, int VV, class T>
+__device__ __forceinline__ float col2im_taps(const T* col, int64_t pitch, int Xo, int y, int x, int u_lo,
+                                             int u_hi, int v_lo, int v_hi) {
+  float acc = 0.f;
+#pragma unroll
+  for (int u = 0; u < UU; ++u) {
+    const T* crow = col + int64_t(u * VV) * pitch + (y - u) * Xo;
+#pragma unroll
+    for (int vv = 0; vv < VV; ++vv) {
+      const bool ok = u >= u_lo && u <= u_hi && vv >= v_lo && vv <= v_hi;
+      acc += ok ? eld(crow + int64_t(vv) * pitch + (x - vv)) : 0.f;
+    }
+  }
+  return acc;
+}
 
 template <class T>
 __global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __restrict__ ds, int n) {
@@ -314,50 +334,58 @@ __global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __re
     const T* src0 = reinterpret_cast<const T*>(d.a.ptr) + c * d.a.st[1] + u * d.a.st[2] + v * d.a.st[3];
     T* dst0 = reinterpret_cast<T*>(d.out) + int64_t(k) * pitch;
     const int r0 = rb * kRowsPerBlock + warp * kRowsPerWarp;
+    const int r1 = min(R, r0 + kRowsPerWarp);
+    // (nb, y) of the warp's first row once; then incremented row by row (no divisions)
+    int nb0 = r0 / Yo, y0 = r0 - nb0 * Yo;
     for (int x0 = 0; x0 < Xo; x0 += 32) {
       const int x = x0 + lane;
-      float val[kRowsPerWarp];
-      T* dst[kRowsPerWarp];
+      int nb = nb0, y = y0;
+      for (int r = r0; r < r1; r += 8) {
+        float val[8];
+        T* dst[8];
 #pragma unroll
-      for (int j = 0; j < kRowsPerWarp; ++j) {
-        const int r = r0 + j;
-        dst[j] = nullptr;
-        val[j] = 0.f;
-        if (r < R && x < Xo) {
-          const int nb = r / Yo, y = r - nb * Yo;
-          val[j] = eld(src0 + nb * d.a.st[0] + y * d.a.st[2] + x * d.a.st[3]);
-          dst[j] = dst0 + nb * img + y * Xo + x;
+        for (int j = 0; j < 8; ++j) {
+          dst[j] = nullptr;
+          val[j] = 0.f;
+          if (r + j < r1 && x < Xo) {
+            val[j] = eld(src0 + nb * d.a.st[0] + y * d.a.st[2] + x * d.a.st[3]);
+            dst[j] = dst0 + nb * img + y * Xo + x;
+          }
+          if (++y == Yo) { y = 0; ++nb; }
         }
-      }
 #pragma unroll
-      for (int j = 0; j < kRowsPerWarp; ++j)
-        if (dst[j]) est(dst[j], val[j]);
+        for (int j = 0; j < 8; ++j)
+          if (dst[j]) est(dst[j], val[j]);
+      }
     }
   } else {
-    // block = ((nb, c), chunk of kRowsPerBlock y rows); per output element
+    // block = ((nb, c), chunk of kColRowsPerBlock y rows); per output element
     //   out[nb, c, y, x] = sum_{u,v} col[(c,u,v)*pitch + nb*img + (y-u)*Xo + (x-v)]
     const int C = int(d.p[0]), U = int(d.p[1]), V = int(d.p[2]), Yo = int(d.p[3]), Xo = int(d.p[4]);
     const int64_t pitch = d.p[5], img = d.p[6];
     const int H = Yo + U - 1, W = Xo + V - 1;
-    const int nblk = (H + kRowsPerBlock - 1) / kRowsPerBlock;
+    const int nblk = (H + kColRowsPerBlock - 1) / kColRowsPerBlock;
     const int nc = tile / nblk, yb = tile - nc * nblk;
     const int c = nc % C, nb = nc / C;
     const T* col = reinterpret_cast<const T*>(d.a.ptr) + int64_t(nb) * img + int64_t(c * U * V) * pitch;
     T* out = reinterpret_cast<T*>(d.out) + int64_t(nc) * H * W;
-    const int y0 = yb * kRowsPerBlock + warp * kRowsPerWarp;
-    for (int j = 0; j < kRowsPerWarp; ++j) {
+    const int y0 = yb * kColRowsPerBlock + warp * kColRowsPerWarp;
+    for (int j = 0; j < kColRowsPerWarp; ++j) {
       const int y = y0 + j;
       if (y >= H) break;
+      const int u_lo = max(0, y - Yo + 1), u_hi = min(U - 1, y);
       for (int x = lane; x < W; x += 32) {
+        const int v_lo = max(0, x - Xo + 1), v_hi = min(V - 1, x);
         float acc = 0.f;
-        for (int u = 0; u < U; ++u) {
-          const int yy = y - u;
-          if (yy < 0 || yy >= Yo) continue;
-          const T* crow = col + int64_t(u * V) * pitch + yy * Xo;
+        if (U == 3 && V == 3) {
+          acc = col2im_taps<3, 3>(col, pitch, Xo, y, x, u_lo, u_hi, v_lo, v_hi);
+        } else if (U == 5 && V == 5) {
+          acc = col2im_taps<5, 5>(col, pitch, Xo, y, x, u_lo, u_hi, v_lo, v_hi);
+        } else {
+          for (int u = u_lo; u <= u_hi; ++u) {
+            const T* crow = col + int64_t(u * V) * pitch + (y - u) * Xo;
 #pragma unroll 4
-          for (int vv = 0; vv < V; ++vv) {
-            const int xx = x - vv;
-            if (xx >= 0 && xx < Xo) acc += eld(crow + int64_t(vv) * pitch + xx);
+            for (int vv = v_lo; vv <= v_hi; ++vv) acc += eld(crow + int64_t(vv) * pitch + (x - vv));
           }
         }
         est(out + int64_t(y) * W + x, acc);
@@ -540,9 +568,9 @@ void conv_prepare(ConvBatch& b) {
       if (d.mode == CONV_IM2COL) {  // K x ceil(N*Yo / rpb) blocks
         const int64_t K = d.a.shape[1] * d.p[0] * d.p[1];
         tiles += K * ((d.a.shape[0] * d.p[2] + rpb - 1) / rpb);
-      } else {                      // N*C x ceil(H / rpb) blocks
+      } else {                      // N*C x ceil(H / rows per block) blocks
         const int64_t H = d.p[3] + d.p[1] - 1;
-        tiles += d.a.shape[0] * d.p[0] * ((H + rpb - 1) / rpb);
+        tiles += d.a.shape[0] * d.p[0] * ((H + kColRowsPerBlock - 1) / kColRowsPerBlock);
       }
     } else {
       tiles += (d.n + kThreads - 1) / kThreads;
