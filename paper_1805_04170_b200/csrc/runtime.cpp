@@ -80,7 +80,13 @@ struct Lowerer {
   std::vector<int> defer_to;   // concat node index a fetch/slice is pasted into, or -1
   std::vector<char> is_holder;
   std::vector<int> pending;    // open class producing the node, or -1
-  std::map<int, std::pair<int, int>> chain_tail;  // node -> (gemm batch, problem)
+  // node -> (gemm batch, [(problem, element offset of the problem's output in the node)]):
+  // the launch an elementwise consumer of the node can be fused into
+  struct Tail {
+    int batch;
+    std::vector<std::pair<int, int64_t>> probs;
+  };
+  std::map<int, Tail> chain_tail;
   std::vector<int> gemm_step;  // gemm batch -> step index (-1 while open)
 
   // open segment
@@ -241,7 +247,7 @@ struct Lowerer {
       s.c_cs = 1;
       auto& specs = prog.gemm_specs[size_t(o_gemm)];
       specs.push_back(s);
-      chain_tail[ni] = {o_gemm, int(specs.size()) - 1};
+      chain_tail[ni] = Tail{o_gemm, {{int(specs.size()) - 1, 0}}};
       const double M = double(op.ta ? s.a.cols : s.a.rows), K = double(op.ta ? s.a.rows : s.a.cols);
       const double N = double(op.tb ? s.b.rows : s.b.cols);
       P.gemm_flops += 2.0 * M * N * K;
@@ -385,6 +391,7 @@ struct Lowerer {
       const int64_t img = pitch4(YX);
       float* col = im2col(a, U, V, Yo, Xo, img, ld);
       const MatView km = filter(b);
+      Tail tail{o_gemm, {}};
       for (int64_t i = 0; i < NB; ++i) {
         GemmSpec s;
         s.a = km;
@@ -392,7 +399,9 @@ struct Lowerer {
         s.c = eoff(out.ptr, i * O * YX);
         s.c_rs = YX;
         specs.push_back(s);
+        tail.probs.push_back({int(specs.size()) - 1, i * O * YX});
       }
+      if (fuse) chain_tail[ni] = tail;  // act(z) runs in these problems' epilogues
       flops = 2.0 * double(NB) * double(O) * double(YX) * double(K);
     } else if (op.mode == ConvMode::grad_weight) {
       // gk[o, cuv] = Gp[o, (n,yx)] . col[cuv, (n,yx)]^T
@@ -482,10 +491,11 @@ struct Lowerer {
       }
     if (j_tail < 0) return false;
     const int src = n.sources[size_t(j_tail)];
-    const auto bp = chain_tail[src];
-    auto& spec = prog.gemm_specs[size_t(bp.first)][size_t(bp.second)];
-    if (spec.n_epi >= kMaxEpi) return false;
-    const int gstep = gemm_step[size_t(bp.first)];
+    const Tail tail = chain_tail[src];
+    const bool multi = tail.probs.size() > 1 || pl.nodes[size_t(src)].region.shape().size() != 2;  // conv
+    for (const auto& pp : tail.probs)
+      if (prog.gemm_specs[size_t(tail.batch)][size_t(pp.first)].n_epi >= kMaxEpi) return false;
+    const int gstep = gemm_step[size_t(tail.batch)];
     EpiStage st;
     switch (op.fn) {
       case EwFn::pointwise_fn: st.op = EPI_TANH; break;
@@ -495,6 +505,7 @@ struct Lowerer {
       case EwFn::sub: st.op = j_tail == 0 ? EPI_SUB_PO : EPI_SUB_OP; break;
     }
     if (n.sources.size() == 2) {
+      if (multi) return false;
       const int other = n.sources[size_t(1 - j_tail)];
       if (other == src) return false;
       if (pending[size_t(other)] >= 0) return false;  // produced by an open launch
@@ -508,12 +519,17 @@ struct Lowerer {
     }
     const StridedView out = alloc(n.region.shape());
     set_val(ni, out);
-    st.out = out.ptr;
-    st.out_rs = out.st[0];
-    st.out_cs = 1;
-    spec.epi[spec.n_epi++] = st;
+    for (const auto& pp : tail.probs) {
+      auto& spec = prog.gemm_specs[size_t(tail.batch)][size_t(pp.first)];
+      EpiStage e = st;
+      // the fused output has the node's (contiguous) layout, like the problem's own output
+      e.out = eoff(out.ptr, pp.second);
+      e.out_rs = spec.c_rs;
+      e.out_cs = 1;
+      spec.epi[spec.n_epi++] = e;
+    }
     chain_tail.erase(src);
-    chain_tail[ni] = bp;
+    chain_tail[ni] = tail;
     P.n_fused++;
     if (gstep >= 0) {
       P.avail_step[size_t(ni)] = gstep;
