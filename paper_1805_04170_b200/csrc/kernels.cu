@@ -289,108 +289,179 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(const ConvDesc* __restri
   est(reinterpret_cast<T*>(d.out) + e, acc);
 }
 
-// im2col / col2im of the tensor-core conv lowering: one warp per output row (lanes over x), so
-// reads and writes are coalesced and the index decomposition is paid once per row.
-constexpr int kRowsPerWarp = 32;     // im2col rows per warp (incremental row indices)
-constexpr int kColRowsPerWarp = 2;   // col2im output rows per warp (U*V taps each)
-constexpr int kColRowsPerBlock = (kThreads / 32) * kColRowsPerWarp;
+// im2col / col2im of the tensor-core conv lowering.
+//   im2col: block = (channel c, group of G images, chunk of taps).  The block stages the G input
+//     planes a[n, c, :, :] in shared memory once (read from HBM once), then writes every tap's
+//     column segment: thread items run over the group's flat (image, y, x) output positions, so
+//     each warp store is one contiguous run of a column row and the (y, x) decomposition is paid
+//     once per item, not per tap.  HBM traffic = input planes + columns (write-bound).
+//   col2im: block = (channel c, group of G images); thread items over the flat (image, y, x)
+//     output positions; each tap's read is a contiguous run of a column row (coalesced), taps
+//     summed in ascending (u, v) order (the direct conv's order), optional fused 1 - tanh^2.
+constexpr int kMoveSmem = 32768;  // im2col plane staging per block (bytes)
 
-// Sum of the valid taps of a UxV filter for one col2im output element, fixed trip counts and
-// predicated loads, in (u, v) order (the direct conv's order).
-template <int UU, int VV, class T>
-__device__ __forceinline__ float col2im_taps(const T* col, int64_t pitch, int Xo, int y, int x, int u_lo,
-                                             int u_hi, int v_lo, int v_hi) {
+// Sum of the valid taps of one col2im output element in ascending tap order: p0 = the element's
+// column position, ctoff[t] = tap t's offset from it, bit t of `mask` = tap t lands inside.
+template <int NT, class T>
+__device__ __forceinline__ float col2im_masked(const T* p0, const long long* ctoff, uint32_t mask, int nt) {
   float acc = 0.f;
+  if constexpr (NT > 0) {
 #pragma unroll
-  for (int u = 0; u < UU; ++u) {
-    const T* crow = col + int64_t(u * VV) * pitch + (y - u) * Xo;
-#pragma unroll
-    for (int vv = 0; vv < VV; ++vv) {
-      const bool ok = u >= u_lo && u <= u_hi && vv >= v_lo && vv <= v_hi;
-      acc += ok ? eld(crow + int64_t(vv) * pitch + (x - vv)) : 0.f;
-    }
+    for (int t = 0; t < NT; ++t) acc += (mask >> t) & 1u ? eld(p0 + ctoff[t]) : 0.f;
+  } else {
+#pragma unroll 4
+    for (int t = 0; t < nt; ++t) acc += (mask >> t) & 1u ? eld(p0 + ctoff[t]) : 0.f;
   }
   return acc;
 }
 
+constexpr int kMaxTapChunk = 128;  // taps per im2col block (offset table in shared memory)
+constexpr int kIm2colIlp = 4;      // items per thread in flight
+
+// Column segments of `nt` taps for Gn images: item (g, y, x) of the flat output positions reads
+// base[g*is + y*rs + x*cs + toff[t]] and writes dst[t*pitch + g*img + y*Xo + x].  Offsets are
+// computed once per item; the tap loop is a shared-memory (or L1) load and a store per element.
 template <class T>
-__global__ void __launch_bounds__(kThreads) convmove_kernel(const ConvDesc* __restrict__ ds, int n) {
+__device__ __forceinline__ void im2col_items(const T* __restrict__ base, int is, int rs, int cs,
+                                             const int* toff, int nt, int Gn, int YX, int Xo,
+                                             int64_t img, int64_t pitch, T* __restrict__ dst) {
+  const int n_items = Gn * YX;
+  for (int it0 = threadIdx.x; it0 < n_items; it0 += kThreads * kIm2colIlp) {
+    int so[kIm2colIlp], dof[kIm2colIlp];
+#pragma unroll
+    for (int j = 0; j < kIm2colIlp; ++j) {
+      const int it = it0 + j * kThreads;
+      const int g = it / YX, e = it - g * YX, y = e / Xo, x = e - y * Xo;
+      so[j] = g * is + y * rs + x * cs;
+      dof[j] = it < n_items ? int(g * img) + e : -1;
+    }
+    T* dp = dst;
+#pragma unroll 2
+    for (int t = 0; t < nt; ++t) {
+      const int to = toff[t];
+      T v[kIm2colIlp];
+#pragma unroll
+      for (int j = 0; j < kIm2colIlp; ++j)
+        if (dof[j] >= 0) v[j] = base[so[j] + to];
+#pragma unroll
+      for (int j = 0; j < kIm2colIlp; ++j)
+        if (dof[j] >= 0) dp[dof[j]] = v[j];
+      dp += pitch;
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) im2col_kernel(const ConvDesc* __restrict__ ds, int n) {
+  //   out[(c*U*V + u*V + v)*pitch + nb*img + y*Xo + x] = a[nb, c, y+u, x+v]
+  extern __shared__ __align__(16) unsigned char move_smem[];
+  __shared__ int toff[kMaxTapChunk];  // tap (u, v) -> source offset
   const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
   const ConvDesc& d = ds[di];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kRowsPerBlock = (kThreads / 32) * kRowsPerWarp;
   const int tile = int(int64_t(blockIdx.x) - d.tile_begin);
   const int NB = int(d.a.shape[0]);
-  if (d.mode == CONV_IM2COL) {
-    // block = (k, chunk of kRowsPerBlock (nb, y) rows); per row
-    //   out[k*pitch + nb*img + y*Xo + x] = a[nb, c, y+u, x+v]
-    // the index decomposition of k is paid once per block, of (nb, y) once per row (32-bit),
-    // and a warp's rows issue their loads together
-    const int U = int(d.p[0]), V = int(d.p[1]), Yo = int(d.p[2]), Xo = int(d.p[3]);
-    const int64_t pitch = d.p[4], img = d.p[5];
-    const int R = NB * Yo, nblk = (R + kRowsPerBlock - 1) / kRowsPerBlock;
-    const int k = tile / nblk, rb = tile - k * nblk;
-    const int v = k % V, u = (k / V) % U, c = k / (U * V);
-    const T* src0 = reinterpret_cast<const T*>(d.a.ptr) + c * d.a.st[1] + u * d.a.st[2] + v * d.a.st[3];
-    T* dst0 = reinterpret_cast<T*>(d.out) + int64_t(k) * pitch;
-    const int r0 = rb * kRowsPerBlock + warp * kRowsPerWarp;
-    const int r1 = min(R, r0 + kRowsPerWarp);
-    // (nb, y) of the warp's first row once; then incremented row by row (no divisions)
-    int nb0 = r0 / Yo, y0 = r0 - nb0 * Yo;
-    for (int x0 = 0; x0 < Xo; x0 += 32) {
-      const int x = x0 + lane;
-      int nb = nb0, y = y0;
-      for (int r = r0; r < r1; r += 8) {
-        float val[8];
-        T* dst[8];
+  const int U = int(d.p[0]), V = int(d.p[1]), Yo = int(d.p[2]), Xo = int(d.p[3]);
+  const int64_t pitch = d.p[4], img = d.p[5];
+  const int TC = int(d.p[6]), G = max(1, int(d.p[7]));  // p[7] = 0: planes read from global
+  const int H = Yo + U - 1, W = Xo + V - 1, HW = H * W, YX = Yo * Xo, UV = U * V;
+  const int ngrp = (NB + G - 1) / G, nch = (UV + TC - 1) / TC;
+  const int c = tile / (ngrp * nch), rest = tile - c * ngrp * nch;
+  const int gb = rest / nch, ch = rest - gb * nch;
+  const int nb0 = gb * G, Gn = min(G, NB - nb0);
+  const int k0 = ch * TC, k1 = min(UV, k0 + TC);
+  const T* src = reinterpret_cast<const T*>(d.a.ptr) + int64_t(nb0) * d.a.st[0] + int64_t(c) * d.a.st[1];
+  T* dst = reinterpret_cast<T*>(d.out) + int64_t(c * UV + k0) * pitch + int64_t(nb0) * img;
+  if (d.p[7] > 0) {
+    T* sp = reinterpret_cast<T*>(move_smem);
+    if (d.a.st[3] == 1 && d.a.st[2] == W) {
+      // dense planes: 4 independent loads in flight per thread, no index decomposition
+      for (int g = 0; g < Gn; ++g) {
+        const T* pl = src + int64_t(g) * d.a.st[0];
+        T* sq = sp + g * HW;
+        for (int i = threadIdx.x; i < HW; i += 4 * kThreads) {
+          T v[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          dst[j] = nullptr;
-          val[j] = 0.f;
-          if (r + j < r1 && x < Xo) {
-            val[j] = eld(src0 + nb * d.a.st[0] + y * d.a.st[2] + x * d.a.st[3]);
-            dst[j] = dst0 + nb * img + y * Xo + x;
-          }
-          if (++y == Yo) { y = 0; ++nb; }
+          for (int j = 0; j < 4; ++j)
+            if (i + j * kThreads < HW) v[j] = pl[i + j * kThreads];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (i + j * kThreads < HW) sq[i + j * kThreads] = v[j];
         }
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (dst[j]) est(dst[j], val[j]);
+      }
+    } else {
+      for (int i = threadIdx.x; i < Gn * HW; i += kThreads) {
+        const int g = i / HW, r = i - g * HW, y = r / W, x = r - y * W;
+        sp[i] = src[int64_t(g) * d.a.st[0] + int64_t(y) * d.a.st[2] + int64_t(x) * d.a.st[3]];
       }
     }
-  } else {
-    // block = ((nb, c), chunk of kColRowsPerBlock y rows); per output element
-    //   out[nb, c, y, x] = sum_{u,v} col[(c,u,v)*pitch + nb*img + (y-u)*Xo + (x-v)]
-    const int C = int(d.p[0]), U = int(d.p[1]), V = int(d.p[2]), Yo = int(d.p[3]), Xo = int(d.p[4]);
-    const int64_t pitch = d.p[5], img = d.p[6];
-    const int H = Yo + U - 1, W = Xo + V - 1;
-    const int nblk = (H + kColRowsPerBlock - 1) / kColRowsPerBlock;
-    const int nc = tile / nblk, yb = tile - nc * nblk;
-    const int c = nc % C, nb = nc / C;
-    const T* col = reinterpret_cast<const T*>(d.a.ptr) + int64_t(nb) * img + int64_t(c * U * V) * pitch;
-    T* out = reinterpret_cast<T*>(d.out) + int64_t(nc) * H * W;
-    const int y0 = yb * kColRowsPerBlock + warp * kColRowsPerWarp;
-    for (int j = 0; j < kColRowsPerWarp; ++j) {
-      const int y = y0 + j;
-      if (y >= H) break;
-      const int u_lo = max(0, y - Yo + 1), u_hi = min(U - 1, y);
-      for (int x = lane; x < W; x += 32) {
-        const int v_lo = max(0, x - Xo + 1), v_hi = min(V - 1, x);
-        float acc = 0.f;
-        if (U == 3 && V == 3) {
-          acc = col2im_taps<3, 3>(col, pitch, Xo, y, x, u_lo, u_hi, v_lo, v_hi);
-        } else if (U == 5 && V == 5) {
-          acc = col2im_taps<5, 5>(col, pitch, Xo, y, x, u_lo, u_hi, v_lo, v_hi);
-        } else {
-          for (int u = u_lo; u <= u_hi; ++u) {
-            const T* crow = col + int64_t(u * V) * pitch + (y - u) * Xo;
+    for (int k = k0 + threadIdx.x; k < k1; k += kThreads) toff[k - k0] = (k / V) * W + (k % V);
+    __syncthreads();
+    im2col_items<T>(sp, HW, W, 1, toff, k1 - k0, Gn, YX, Xo, img, pitch, dst);
+  } else {  // one image per block, plane read from global (L1/L2)
+    const int rs = int(d.a.st[2]), cs = int(d.a.st[3]);
+    for (int k = k0 + threadIdx.x; k < k1; k += kThreads) toff[k - k0] = (k / V) * rs + (k % V) * cs;
+    __syncthreads();
+    im2col_items<T>(src, 0, rs, cs, toff, k1 - k0, 1, YX, Xo, img, pitch, dst);
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads, 4) col2im_kernel(const ConvDesc* __restrict__ ds, int n) {
+  //   out[nb, c, y, x] = sum_{u,v} col[(c,u,v)*pitch + nb*img + (y-u)*Xo + (x-v)]
+  //   (b.ptr != null: also writes 1 - tanh(out)^2 there, from the stored value)
+  __shared__ long long ctoff[32];
+  const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
+  const ConvDesc& d = ds[di];
+  const int tile = int(int64_t(blockIdx.x) - d.tile_begin);
+  const int NB = int(d.a.shape[0]);
+  const int C = int(d.p[0]), U = int(d.p[1]), V = int(d.p[2]), Yo = int(d.p[3]), Xo = int(d.p[4]);
+  const int64_t pitch = d.p[5], img = d.p[6];
+  const int G = int(d.p[7]);
+  const int H = Yo + U - 1, W = Xo + V - 1, HW = H * W, UV = U * V;
+  const int ngrp = (NB + G - 1) / G;
+  const int c = tile / ngrp, gb = tile - c * ngrp;
+  const int nb0 = gb * G, Gn = min(G, NB - nb0);
+  const T* col0 = reinterpret_cast<const T*>(d.a.ptr) + int64_t(nb0) * img + int64_t(c * U * V) * pitch;
+  T* out0 = reinterpret_cast<T*>(d.out) + (int64_t(nb0) * C + c) * HW;
+  T* dact0 = d.b.ptr ? reinterpret_cast<T*>(d.b.ptr) + (int64_t(nb0) * C + c) * HW : nullptr;
+  for (int t = threadIdx.x; t < min(UV, 32); t += kThreads) ctoff[t] = t * pitch - (t / V) * Xo - (t % V);
+  __syncthreads();
+  // item (g, y, x) advanced by kThreads per iteration without divisions
+  const int dy = kThreads / W, dx = kThreads - dy * W;
+  int g = threadIdx.x / HW, r0 = threadIdx.x - g * HW;
+  int y = r0 / W, x = r0 - y * W;
+  for (; g < Gn;) {
+    const T* col = col0 + int64_t(g) * img;
+    const int u_lo = max(0, y - Yo + 1), u_hi = min(U - 1, y);
+    const int v_lo = max(0, x - Xo + 1), v_hi = min(V - 1, x);
+    float acc = 0.f;
+    if (UV <= 32) {
+      const uint32_t vb = (2u << v_hi) - (1u << v_lo);
+      uint32_t mask = 0;
+      for (int u = u_lo; u <= u_hi; ++u) mask |= vb << (u * V);
+      const T* p0 = col + y * Xo + x;
+      if (UV == 9) acc = col2im_masked<9>(p0, ctoff, mask, UV);
+      else if (UV == 25) acc = col2im_masked<25>(p0, ctoff, mask, UV);
+      else acc = col2im_masked<0>(p0, ctoff, mask, UV);
+    } else {
+      for (int u = u_lo; u <= u_hi; ++u) {
+        const T* crow = col + int64_t(u * V) * pitch + (y - u) * Xo;
 #pragma unroll 4
-            for (int vv = v_lo; vv <= v_hi; ++vv) acc += eld(crow + int64_t(vv) * pitch + (x - vv));
-          }
-        }
-        est(out + int64_t(y) * W + x, acc);
+        for (int vv = v_lo; vv <= v_hi; ++vv) acc += eld(crow + int64_t(vv) * pitch + (x - vv));
       }
     }
+    const int64_t o = int64_t(g) * C * HW + y * W + x;
+    est(out0 + o, acc);
+    if (dact0) {
+      float h = acc;  // the stored value
+      if constexpr (sizeof(T) == 2) h = __bfloat162float(__float2bfloat16_rn(acc));
+      const float t = tanhf(h);
+      est(dact0 + o, 1.0f - t * t);
+    }
+    x += dx;
+    y += dy;
+    if (x >= W) { x -= W; ++y; }
+    while (y >= H) { y -= H; ++g; }
   }
 }
 
@@ -560,17 +631,35 @@ void init_free(InitBatch& b) {
 void conv_prepare(ConvBatch& b) {
   int64_t tiles = 0;
   b.move = !b.descs.empty() && b.descs[0].mode >= CONV_IM2COL;
+  b.smem = 0;
+  const int64_t es = b.bf16 ? 2 : 4;
   for (auto& d : b.descs) {
     if ((d.mode >= CONV_IM2COL) != b.move) throw std::runtime_error("conv batch mixes compute and data movement");
+    if (b.move && d.mode != b.descs[0].mode) throw std::runtime_error("conv batch mixes im2col and col2im");
     d.tile_begin = tiles;
     if (b.move) {
-      const int64_t rpb = (kThreads / 32) * kRowsPerWarp;
-      if (d.mode == CONV_IM2COL) {  // K x ceil(N*Yo / rpb) blocks
-        const int64_t K = d.a.shape[1] * d.p[0] * d.p[1];
-        tiles += K * ((d.a.shape[0] * d.p[2] + rpb - 1) / rpb);
-      } else {                      // N*C x ceil(H / rows per block) blocks
-        const int64_t H = d.p[3] + d.p[1] - 1;
-        tiles += d.a.shape[0] * d.p[0] * ((H + kColRowsPerBlock - 1) / kColRowsPerBlock);
+      const int64_t NB = std::max<int64_t>(d.a.shape[0], 1);
+      if (d.mode == CONV_IM2COL) {
+        // G images per block: ~4 items per thread, planes within the staging buffer
+        const int64_t U = d.p[0], V = d.p[1], YX = d.p[2] * d.p[3];
+        const int64_t HW = (d.p[2] + U - 1) * (d.p[3] + V - 1), UV = U * V;
+        int64_t G = std::max<int64_t>(1, (4 * kThreads + YX - 1) / std::max<int64_t>(YX, 1));
+        G = std::min({G, NB, kMoveSmem / (HW * es)});  // 0: plane too large, read from global
+        const int64_t Gb = std::max<int64_t>(G, 1);
+        const int64_t blocks = d.a.shape[1] * ((NB + Gb - 1) / Gb);
+        // split the taps when the (c, group) blocks alone do not fill the GPU
+        const int64_t nch = std::min<int64_t>(UV, std::max<int64_t>(1, (4 * 148 + blocks - 1) / blocks));
+        int64_t TC = (UV + nch - 1) / nch;
+        TC = std::min<int64_t>(TC, kMaxTapChunk);
+        d.p[6] = TC;
+        d.p[7] = G;
+        tiles += blocks * ((UV + TC - 1) / TC);
+        b.smem = std::max<int64_t>(b.smem, G * HW * es);
+      } else {
+        const int64_t HW = (d.p[3] + d.p[1] - 1) * (d.p[4] + d.p[2] - 1);
+        const int64_t G = std::min(NB, std::max<int64_t>(1, (8 * kThreads + HW - 1) / std::max<int64_t>(HW, 1)));
+        d.p[7] = G;
+        tiles += d.p[0] * ((NB + G - 1) / G);
       }
     } else {
       tiles += (d.n + kThreads - 1) / kThreads;
@@ -584,8 +673,12 @@ void conv_run(const ConvBatch& b, cudaStream_t s) {
   if (!b.tiles) return;
   const ConvDesc* ds = static_cast<const ConvDesc*>(b.d_descs);
   const int nd = int(b.descs.size());
-  if (b.move && b.bf16) convmove_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
-  else if (b.move) convmove_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
+  const size_t sm = size_t(b.smem);
+  const bool col2im = b.move && b.descs[0].mode == CONV_COL2IM;
+  if (col2im && b.bf16) col2im_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
+  else if (col2im) col2im_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
+  else if (b.move && b.bf16) im2col_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, sm, s>>>(ds, nd);
+  else if (b.move) im2col_kernel<float><<<unsigned(b.tiles), kThreads, sm, s>>>(ds, nd);
   else if (b.bf16) conv_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
   else conv_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
   CUDA_CHECK(cudaGetLastError());

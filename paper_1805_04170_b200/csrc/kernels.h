@@ -102,7 +102,8 @@ enum ConvModeCode : int {
                          //   pitch >= N*img, 16-byte rows)
   CONV_COL2IM = 5,       // out[n,c,y,x] = sum_{u,v} col[(c*U*V+u*V+v)*pitch + n*img + (y-u)*Xo+(x-v)]
                          //   (a.ptr = col, a.shape[0] = N, p = C,U,V,Yo,Xo,pitch,img; taps in
-                         //   ascending (u, v) order)
+                         //   ascending (u, v) order; b.ptr != null: also b[...] = 1 - tanh(out)^2)
+                         //   p[6..7] = launch geometry, set by conv_prepare
 };
 struct ConvDesc {
   int mode;
@@ -119,6 +120,7 @@ struct ConvBatch {
   int64_t tiles = 0;
   double flops = 0;
   bool move = false;  // im2col / col2im batch (d.n counts rows) rather than direct conv
+  int64_t smem = 0;   // dynamic shared memory of the im2col launch
   bool bf16 = false;  // storage type
 };
 void conv_prepare(ConvBatch& b);

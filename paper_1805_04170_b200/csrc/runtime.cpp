@@ -87,6 +87,13 @@ struct Lowerer {
     std::vector<std::pair<int, int64_t>> probs;
   };
   std::map<int, Tail> chain_tail;
+  // grad_input node -> its col2im descriptor (open batch: desc index; emitted: conv batch, desc,
+  // step), where a 1 - tanh^2 consumer is fused
+  std::map<int, int> post_open;
+  struct PostTail {
+    int batch, desc, step;
+  };
+  std::map<int, PostTail> post_tail;
   std::vector<int> gemm_step;  // gemm batch -> step index (-1 while open)
 
   // open segment
@@ -160,7 +167,13 @@ struct Lowerer {
       const int s = add_step(ST_CONV, int(prog.conv.size()) - 1, o_op, "conv");
       for (int n : o_nodes[C_COMPUTE]) P.avail_step[size_t(n)] = s;
     }
+    const int n_post = int(o_post.descs.size());
     emit_conv(o_post, o_op, "col2im", C_POST);
+    if (n_post) {
+      for (const auto& kv : post_open)
+        post_tail[kv.first] = PostTail{int(prog.conv.size()) - 1, kv.second, int(prog.steps.size()) - 1};
+    }
+    post_open.clear();
     emit_nary(o_pack, seg_op, "pack", C_PACK);
     if (!o_xchg.x.empty()) {
       prog.xchg.push_back(std::move(o_xchg));
@@ -460,6 +473,7 @@ struct Lowerer {
       d.n = out.elements() / out.shape[3];  // rows (n, c, y)
       d.p[0] = C; d.p[1] = U; d.p[2] = V; d.p[3] = Yo; d.p[4] = Xo; d.p[5] = ld; d.p[6] = img;
       o_post.descs.push_back(d);
+      if (fuse) post_open[ni] = int(o_post.descs.size()) - 1;
       flops = 2.0 * double(NB) * double(YX) * double(K) * double(O);
     }
     P.gemm_flops += flops;
@@ -483,6 +497,19 @@ struct Lowerer {
 
   bool try_fuse(int ni, const OpSpec& op) {
     const PlanNode& n = pl.nodes[size_t(ni)];
+    if (op.fn == EwFn::pointwise_fn_grad && n.sources.size() == 1 && post_tail.count(n.sources[0])) {
+      // 1 - tanh^2 of a conv grad_input: written by its col2im from the stored value
+      const PostTail pt = post_tail[n.sources[0]];
+      ConvDesc& d = prog.conv[size_t(pt.batch)].descs[size_t(pt.desc)];
+      if (d.b.ptr) return false;
+      const StridedView out = alloc(n.region.shape());
+      set_val(ni, out);
+      d.b.ptr = out.ptr;
+      post_tail.erase(n.sources[0]);
+      P.n_fused++;
+      P.avail_step[size_t(ni)] = pt.step;
+      return true;
+    }
     int j_tail = -1;
     for (size_t j = 0; j < n.sources.size(); ++j)
       if (chain_tail.count(n.sources[j])) {
