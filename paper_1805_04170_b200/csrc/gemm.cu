@@ -44,7 +44,8 @@ constexpr uint32_t kOutStageBytes = 8 * kOutStage;        // <= 8 epilogue warps
 constexpr int kOtherDepth = 4;                            // max operand boxes in flight per warp
 constexpr uint32_t kOtherBox = 8 * kOutStage;             // one box for each of <= 8 epilogue warps
 constexpr uint32_t kSmemMax = 232448;                     // 227 KB opt-in
-constexpr uint32_t kBarBytes = 512;
+constexpr uint32_t kBarBytes = 1024;
+constexpr int kSegQ = 8;  // tile queue depth (dynamic schedules)
 
 enum SegKind : int { SEG_WHOLE = 0, SEG_HEAD = 1, SEG_PART = 2 };
 
@@ -385,10 +386,17 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   uint64_t* tmem_empty = tmem_full + 2;       // [2]
   uint64_t* other_bar = tmem_empty + 2;       // [8 warps][depth]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(other_bar + 8 * kOtherDepth);
+  // dynamic schedule: tile queue filled by the (leader's) producer from a global counter
+  int* seg_q = reinterpret_cast<int*>(tmem_holder + 2);            // [kSegQ]
+  uint64_t* seg_full = reinterpret_cast<uint64_t*>(seg_q + kSegQ);  // [kSegQ]
+  uint64_t* seg_empty = seg_full + kSegQ;                           // [kSegQ] (leader's)
+  const bool dyn = (has_other & 128) != 0;
 
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;  // 0 = MMA leader of the pair
   const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
-  const int s_begin = seg_off[unit], s_end = seg_off[unit + 1];
+  // static: this unit's segments [seg_off[unit], seg_off[unit+1]); dynamic: segments 0..n-1
+  // handed out in order by flags[0] (flags[1] counts finished units, the last one resets both)
+  const int s_begin = dyn ? 0 : seg_off[unit], s_end = dyn ? seg_off[1] : seg_off[unit + 1];
   const int warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -401,6 +409,13 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       mbar_init(&tmem_empty[a], PAIR ? 2 * NEPI : NEPI);  // one arrival per epilogue warp (of both CTAs)
     }
     for (int w = 0; w < 8 * kOtherDepth; ++w) mbar_init(&other_bar[w], 1);
+    // queue slot consumers: MMA thread, epilogue warps, split warps, and the peer's producer
+    // and epilogue warps (remote arrivals)
+    const int n_cons = 1 + NEPI + (SPLIT ? 4 : 0) + (PAIR ? 1 + NEPI : 0);
+    for (int q = 0; q < kSegQ; ++q) {
+      mbar_init(&seg_full[q], 1);
+      mbar_init(&seg_empty[q], n_cons);
+    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -415,6 +430,29 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   // the leader's barriers, as shared::cluster addresses (pair TMA and epilogue arrivals)
   const uint32_t full_lead = PAIR ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
   const uint32_t tmem_empty_lead = PAIR ? mapa_shared(smem_u32(tmem_empty), 0) : smem_u32(tmem_empty);
+  const uint32_t seg_empty_lead = PAIR ? mapa_shared(smem_u32(seg_empty), 0) : smem_u32(seg_empty);
+  // Segment cursor of one role: static walks [s_begin, s_end); dynamic reads the tile queue
+  // (`arrive`: this thread releases the slot for its role).  Returns -1 when done.
+  struct Cursor {
+    int j, si;
+    bool done;
+  };
+  auto next_seg = [&](Cursor& c, bool arrive) -> int {
+    if (!dyn) return c.si < s_end ? c.si++ : -1;
+    if (c.done) return -1;
+    const int slot = c.j % kSegQ;
+    const uint32_t par = uint32_t(c.j / kSegQ) & 1u;
+    if (PAIR && rank != 0) mbar_wait_acq_cluster(&seg_full[slot], par);
+    else mbar_wait(&seg_full[slot], par);
+    const int idx = *reinterpret_cast<volatile int*>(&seg_q[slot]);
+    if (arrive) {
+      if (PAIR && rank != 0) mbar_arrive_cluster_release(seg_empty_lead + slot * 8);
+      else mbar_arrive(&seg_empty[slot]);
+    }
+    ++c.j;
+    if (idx < 0) c.done = true;
+    return idx;
+  };
 
   // One k-block of operands: K-major tiles are one 2-D box; MN-major tiles are 32-wide
   // 128B_BASE32B-swizzled chunks 4096 bytes apart, one 3-D box when the extent allows.
@@ -451,7 +489,25 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     // ---------------- TMA producer
     const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
     uint32_t s = 0, ph = 0;  // ring slot and its phase parity
-    for (int si = s_begin; si < s_end; ++si) {
+    Cursor cur{0, s_begin, false};
+    for (int j = 0;; ++j) {
+      int si;
+      if (dyn && rank == 0) {
+        // fetch the next segment for the unit and publish it (to the peer as well)
+        const int slot = j % kSegQ;
+        mbar_wait(&seg_empty[slot], ((uint32_t(j / kSegQ)) & 1u) ^ 1u);
+        si = int(atomicAdd(&flags[0], 1u));
+        if (si >= s_end) si = -1;
+        seg_q[slot] = si;
+        if constexpr (PAIR) {
+          st_shared_cluster_u32(mapa_shared(smem_u32(&seg_q[slot]), 1), uint32_t(si));
+          mbar_arrive_cluster_release(mapa_shared(smem_u32(&seg_full[slot]), 1));
+        }
+        mbar_arrive(&seg_full[slot]);
+      } else {
+        si = next_seg(cur, true);
+      }
+      if (si < 0) break;
       const GemmSeg sg = segs[si];
       const GemmProblem& pr = probs[sg.prob];
       const int p0 = sg.tp * PBM + int(rank) * BM, q0 = sg.tq * BN + int(rank) * BNH;
@@ -467,7 +523,10 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   } else if (warp == 1 && lane == 0 && rank == 0) {
     // ---------------- MMA issuer (single thread; the pair's leader CTA)
     uint32_t s = 0, ph = 0;  // ring slot and its phase parity
-    for (int si = s_begin, i = 0; si < s_end; ++si, ++i) {
+    Cursor cur{0, s_begin, false};
+    for (int i = 0;; ++i) {
+      const int si = next_seg(cur, true);
+      if (si < 0) break;
       const GemmSeg sg = segs[si];
       const GemmProblem& pr = probs[sg.prob];
       const uint32_t acc = i & 1, aph = (i >> 1) & 1;
@@ -518,7 +577,10 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     // ---------------- 3xTF32 split: hi in place, lo into the stage's second half
     const int tid = threadIdx.x - 256;  // 0..127
     uint32_t s = 0, ph = 0;  // ring slot and its phase parity
-    for (int si = s_begin; si < s_end; ++si) {
+    Cursor cur{0, s_begin, false};
+    for (;;) {
+      const int si = next_seg(cur, lane == 0);
+      if (si < 0) break;
       const GemmSeg sg = segs[si];
       for (int kb = sg.kb0; kb < sg.kb1; ++kb, (++s == uint32_t(STAGES)) ? (s = 0, ph ^= 1) : 0) {
         mbar_wait(&full[s], ph);
@@ -555,15 +617,20 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     uint32_t o_slot = 0, o_phase = 0;  // consumer ring position
     uint32_t i_slot = 0;               // issuer ring position (lane 0)
     const uint64_t o_policy = policy_evict_first();  // the elementwise operand is read once
-    int isi = s_begin, ic0 = c_begin;                 // issue cursor (lane 0)
+    Cursor icur{0, s_begin, false};                   // issue cursor (lane 0)
+    int ic0 = c_begin;
     const void* imap = nullptr;
-    int iq = 0, ip = 0, iQ = 0, iseg = -1;
+    int iq = 0, ip = 0, iQ = 0;
+    bool iseg = false;  // a segment is loaded into the cursor
     auto issue_other = [&]() {
-      for (; isi < s_end; ++isi, ic0 = c_begin) {
-        if (iseg != isi) {
+      for (;; iseg = false) {
+        if (!iseg) {
+          const int isi = next_seg(icur, false);
+          if (isi < 0) return;
           const GemmSeg sg = segs[isi];
           const GemmProblem& pr = probs[sg.prob];
-          iseg = isi;
+          iseg = true;
+          ic0 = c_begin;
           imap = sg.kind == SEG_PART ? nullptr : pr.tmap_other;
           iq = sg.tq * BN;
           ip = sg.tp * PBM + int(rank) * BM + lq * 32;
@@ -582,7 +649,10 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     };
     if ((has_other & 1) && lane == 0)
       for (int d = 0; d < ODEPTH; ++d) issue_other();
-    for (int si = s_begin, i = 0; si < s_end; ++si, ++i) {
+    Cursor cur{0, s_begin, false};
+    for (int i = 0;; ++i) {
+      const int si = next_seg(cur, lane == 0);
+      if (si < 0) break;
       const GemmSeg sg = segs[si];
       const GemmProblem& pr = probs[sg.prob];
       const uint32_t acc = i & 1, aph = (i >> 1) & 1;
@@ -871,6 +941,15 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   tc_fence_before();
   if constexpr (PAIR) cluster_sync();  // both CTAs done with the pair's TMEM and barriers
   else __syncthreads();
+  if (dyn && threadIdx.x == 0 && rank == 0) {
+    // every unit has fetched past the end: the last one re-arms the counter for the next launch
+    const unsigned units = gridDim.x / (PAIR ? 2u : 1u);
+    if (atomicAdd(&flags[1], 1u) == units - 1) {
+      flags[0] = 0u;
+      flags[1] = 0u;
+      __threadfence();
+    }
+  }
   if (warp == 2) {
     tc_fence_after();
     if constexpr (PAIR) tmem_dealloc_pair(tmem_base, TMEM_COLS);
@@ -921,6 +1000,7 @@ const CUtensorMapL2promotion kOtherPromo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, 
                                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
 bool g_no_pair = false;
 int g_max_bn = 0;  // debug: cap the tile width
+bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-in (10,0)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1014,8 +1094,9 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 7) g_other_promo = sbo > 0 ? int(sbo) - 1 : 0;  // (7,n) operand promotion n-1
   if (lbo == 8) g_no_stream = (sbo == 1);  // (8,1) no L2 streaming hints
   if (lbo == 9) g_max_bn = int(sbo);       // (9,n) tile width <= n
+  if (lbo == 10) g_no_dyn = (sbo == 1);    // (10,0) dynamic / (10,1) static whole-tile schedules
   if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
-  if (lbo >= 1 && lbo <= 9) g_dbg_lbo = g_dbg_sbo = 0;
+  if (lbo >= 1 && lbo <= 10) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1288,6 +1369,30 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     }
   }
   g.sched = gemm_schedule(probs, g.bn, g.pair ? num_sms / 2 : num_sms, 0);
+  if (!g.sched.stream_k && !g_no_dyn) {
+    // Whole tiles only: hand them out in order from a device counter instead of fixed per-CTA
+    // lists, so SMs that run ahead (less contention, nearer memory) take more tiles and the
+    // launch ends with the slowest SM's last tile, not its share.  Order: (problem, tq, tp), so
+    // the tiles in flight at any moment share their Q panels and sweep the P operand.
+    std::vector<GemmSeg> order;
+    for (int pi = 0; pi < int(probs.size()); ++pi)
+      for (int tq = 0; tq < probs[size_t(pi)].tiles_q; ++tq)
+        for (int tp = 0; tp < probs[size_t(pi)].tiles_p; ++tp) {
+          GemmSeg sg;
+          sg.prob = pi;
+          sg.tp = tp;
+          sg.tq = tq;
+          sg.kb0 = 0;
+          sg.kb1 = probs[size_t(pi)].kb_total;
+          sg.kind = SEG_WHOLE;
+          order.push_back(sg);
+        }
+    g.sched.segs = order;
+    g.sched.seg_off = {0, int(order.size())};
+    g.sched.dynamic = true;
+    const int units = g.pair ? num_sms / 2 : num_sms;
+    g.sched.grid = std::max(1, std::min<int>(units, int(order.size())));
+  }
   g.units = g.sched.grid * (g.pair ? 2 : 1);
   const size_t halves = size_t(g.sched.nslots) * (g.pair ? 2 : 1);  // one BM x BN slot per CTA
   g.ws_floats = halves * BM * g.bn;
@@ -1295,6 +1400,9 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     CUDA_CHECK(cudaMalloc(&g.d_ws, g.ws_floats * sizeof(float)));
     CUDA_CHECK(cudaMalloc(&g.d_flags, halves * sizeof(unsigned)));
     CUDA_CHECK(cudaMemset(g.d_flags, 0, halves * sizeof(unsigned)));
+  } else if (g.sched.dynamic) {
+    CUDA_CHECK(cudaMalloc(&g.d_flags, 2 * sizeof(unsigned)));  // tile counter, finished units
+    CUDA_CHECK(cudaMemset(g.d_flags, 0, 2 * sizeof(unsigned)));
   }
   const size_t nload = maps.size();
   maps.insert(maps.end(), store_maps.begin(), store_maps.end());
@@ -1339,7 +1447,7 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair, g.bf16);
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
-  const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4);
+  const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0);
   if (g.pair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * g.sched.grid));

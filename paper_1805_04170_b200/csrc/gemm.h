@@ -72,6 +72,7 @@ struct GemmSchedule {
   int nslots = 0;               // partial-tile workspace slots
   std::vector<GemmSeg> segs;    // all CTAs' lists, concatenated
   std::vector<int> seg_off;     // CTA c owns segs[seg_off[c], seg_off[c+1])
+  bool dynamic = false;         // segs handed out in order by a device counter (seg_off = {0, n})
 };
 
 // Host-side description of one sub-op matmul over strided row-major fp32 views.

@@ -112,6 +112,7 @@ struct Lowerer {
         fuse(p.flags & 1), force_xchg(p.flags & 2), tc_conv(!(p.flags & 4)) {}
   bool tc_conv;
   std::map<std::vector<int64_t>, float*> col_cache;  // im2col buffers by (view, filter) key
+  std::map<std::vector<int64_t>, float*> gp_cache;   // permuted conv gradients by (view, pitch)
 
   float* alloc_bytes(size_t bytes) {
     const size_t off = (P.arena_used + kAlign - 1) / kAlign * kAlign;
@@ -335,7 +336,7 @@ struct Lowerer {
   // Convolution sub-op on the tensor cores (run_conv, proj/src/dense.cpp:92-157):
   //   forward      out[n,o,:,:]  = Kmat[o, cuv] . im2col(a)[n][yx, cuv]^T    per image
   //   grad_weight  gk[o, cuv]    = Gp[o, (n,yx)] . im2col(a)[cuv, (n,yx)]^T  one GEMM
-  //   grad_input   dcol[n][yx,cuv] = G_n^T . Kmat, then col2im (ordered tap sum)
+  //   grad_input   dcol[cuv, (n,yx)] = Kmat^T . Gp, then col2im (ordered tap sum)
   // The im2col / permute copies run in the pre class, col2im in the post class.  Every scratch
   // matrix has 16-byte rows (TMA); padding columns lie outside the tensor maps.
   void lower_conv_gemm(int ni, const OpSpec& op) {
@@ -423,17 +424,7 @@ struct Lowerer {
       int64_t ld = 0;
       const int64_t img = pitch4(YX);
       float* col = im2col(a, U, V, Yo, Xo, img, ld);  // shared with the layer's forward
-      // G[n, o, y, x] -> Gp[o][(n, img-strided y, x)] (padding columns stay 0: zeroed arena)
-      if (!o_pre.descs.empty() && o_pre_op != op.id) flush();
-      o_pre_op = op.id;
-      float* gp = alloc_bytes(size_t(O * ld) * size_t(g_es));
-      StridedView src = b, dst = b;
-      src.shape[0] = O; src.shape[1] = NB;  // permuted view of G: (o, n, y, x)
-      src.st[0] = b.st[1]; src.st[1] = b.st[0];
-      dst.ptr = gp;
-      dst.shape[0] = O; dst.shape[1] = NB;
-      dst.st[0] = ld; dst.st[1] = img; dst.st[2] = Xo; dst.st[3] = 1;
-      o_pre.descs.push_back(ndesc(NARY_COPY, dst, {src}));
+      float* gp = permuted_grad(b, img, ld, op.id);
       GemmSpec s;  // contraction over all images' (padded) columns; pads are 0 in both operands
       s.a = MatView{gp, O, NB * img, ld, 1};
       s.b = MatView{col, K, NB * img, ld, 1};
@@ -443,27 +434,23 @@ struct Lowerer {
       specs.push_back(s);
       flops = 2.0 * double(O) * double(K) * double(NB * YX);
     } else {
-      // dcol[cuv, n*YX + yx] = Kmat[o, cuv]^T . G_n[o, yx]   (one problem per image), then
+      // dcol[cuv, (n, yx)] = Kmat[o, cuv]^T . Gp[o, (n, yx)]   (one GEMM), then
       // col2im: h[n,c,y,x] = sum_{u,v} dcol[(c,u,v), n*YX + (y-u)*Xo + (x-v)]
       const int64_t NB = a.shape[0], O = a.shape[1], Yo = a.shape[2], Xo = a.shape[3];
       const int64_t C = b.shape[1], U = b.shape[2], V = b.shape[3], K = C * U * V, YX = Yo * Xo;
       const MatView km = filter(b);
-      StridedView g = a;
-      const int64_t al = 16 / g_es;  // elements per 16 bytes
-      if (!(g.st[3] == 1 && g.st[2] == Xo && g.st[1] % al == 0 && g.st[0] % al == 0 &&
-            (reinterpret_cast<uintptr_t>(g.ptr) & 15) == 0))
-        g = padded_copy(a, 2, op.id);
       const int64_t img = pitch4(YX), ld = pitch4(NB * img);
+      // dcol = Kmat^T . Gp: one GEMM over every image's (padded) columns; the padding columns of
+      // Gp are 0, so dcol's are too (col2im never reads them)
+      float* gp = permuted_grad(a, img, ld, op.id);
       float* dcol = alloc_bytes(size_t(K * ld) * size_t(g_es));
-      for (int64_t i = 0; i < NB; ++i) {
-        GemmSpec s;
-        s.a = km;                                                // Kmat [o, cuv], used transposed
-        s.ta = true;
-        s.b = MatView{eoff(g.ptr, i * g.st[0]), O, YX, g.st[1], 1};  // G_n [o, yx] (K x N)
-        s.c = eoff(dcol, i * img);
-        s.c_rs = ld;
-        specs.push_back(s);
-      }
+      GemmSpec s;
+      s.a = km;  // Kmat [o, cuv], used transposed
+      s.ta = true;
+      s.b = MatView{gp, O, NB * img, ld, 1};
+      s.c = dcol;
+      s.c_rs = ld;
+      specs.push_back(s);
       ConvDesc d;
       std::memset(&d, 0, sizeof d);
       d.mode = CONV_COL2IM;
@@ -478,6 +465,31 @@ struct Lowerer {
     }
     P.gemm_flops += flops;
     produced(ni, op.mode == ConvMode::grad_input ? C_POST : C_COMPUTE);
+  }
+
+  // G[n, o, y, x] -> Gp[o][(n, img-strided y, x)], rows of `ld` elements (the padding columns
+  // stay 0: zeroed arena), shared by a layer's grad_weight and grad_input (pre class).
+  float* permuted_grad(const StridedView& g, int64_t img, int64_t ld, const std::string& op) {
+    std::vector<int64_t> key = {int64_t(reinterpret_cast<uintptr_t>(g.ptr)), img, ld};
+    for (int i = 0; i < g.rank; ++i) {
+      key.push_back(g.shape[i]);
+      key.push_back(g.st[i]);
+    }
+    auto hit = gp_cache.find(key);
+    if (hit != gp_cache.end()) return hit->second;
+    if (!o_pre.descs.empty() && o_pre_op != op) flush();
+    o_pre_op = op;
+    const int64_t NB = g.shape[0], O = g.shape[1], Xo = g.shape[3];
+    float* gp = alloc_bytes(size_t(O * ld) * size_t(g_es));
+    gp_cache[key] = gp;
+    StridedView src = g, dst = g;
+    src.shape[0] = O; src.shape[1] = NB;  // permuted view of G: (o, n, y, x)
+    src.st[0] = g.st[1]; src.st[1] = g.st[0];
+    dst.ptr = gp;
+    dst.shape[0] = O; dst.shape[1] = NB;
+    dst.st[0] = ld; dst.st[1] = img; dst.st[2] = Xo; dst.st[3] = 1;
+    o_pre.descs.push_back(ndesc(NARY_COPY, dst, {src}));
+    return gp;
   }
 
   StridedView materialize(int node, const std::string& op) {

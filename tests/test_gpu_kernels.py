@@ -64,3 +64,23 @@ def test_gemm_act_epilogue_bitexact():
     import torch
     C, ref, _, (h,) = _run(256, 512, 128, False, False, 1, epi=[1])
     assert torch.equal(h, torch.tanh(C)) or (h - torch.tanh(C)).abs().max().item() <= 2e-7
+
+
+@pytest.mark.parametrize("shape,epi", [((1024, 4096, 256, True, False), [3, 6]), ((512, 1024, 1024, False, True), [1]),
+                                       ((64, 1024, 1024, False, False), None), ((1000, 136, 72, True, True), None)],
+                         ids=["pair_update", "pair_act", "small", "edge"])
+def test_gemm_dynamic_schedule(shape, epi):
+    """Whole-tile schedules handed out by the device tile counter (debug knob (10, 0)):
+    same results as the static per-CTA lists, twice in a row (the counter re-arms itself)."""
+    import torch
+    from paper_1805_04170_b200 import native
+    base = _run(*shape, 0, epi=epi)
+    native.lib().tpx_debug_gemm_mn_desc(10, 0)
+    try:
+        for _ in range(2):
+            got = _run(*shape, 0, epi=epi)
+            assert torch.equal(got[0], base[0])
+            for a, b in zip(got[3], base[3]):
+                assert torch.equal(a, b)
+    finally:
+        native.lib().tpx_debug_gemm_mn_desc(10, 1)

@@ -318,3 +318,32 @@ def test_graph_replay_with_nccl_exchange(ctx):
     for hs in P["holders"].values():
         for hid in hs:
             assert np.array_equal(a.read_node(hid), b.read_node(hid)), hid
+
+
+@pytest.mark.parametrize("stem", [s for s in STEMS if "cfg2r_mlp5x256_b64.opt.k1" in s or "alexr_conv_b4.opt.k1" in s], ids=stem_id)
+def test_dynamic_schedule_rearms(ctx, stem):
+    """Plans prepared with the device tile-counter schedule (gemm debug knob (10, 0)) executed
+    twice on different inputs: the second step's values equal a static-schedule step on the
+    second inputs, so every GEMM re-armed its counter (a stale counter would skip all tiles)."""
+    from paper_1805_04170_b200 import native
+    from paper_1805_04170_b200.executor import PlanExecutor
+    text, P, seed, _, _ = oracle_values(stem)
+    native.lib().tpx_debug_gemm_mn_desc(10, 0)
+    try:
+        dyn = PlanExecutor(ctx, text, precision=0, flags=1)
+    finally:
+        native.lib().tpx_debug_gemm_mn_desc(10, 1)
+    ref = PlanExecutor(ctx, text, precision=0, flags=1)
+    dyn.init_inputs(seed + 1)
+    dyn.execute()
+    dyn.init_inputs(seed)
+    dyn.execute()
+    ref.init_inputs(seed)
+    ref.execute()
+    dyn.synchronize()
+    ref.synchronize()
+    for t, hs in P["holders"].items():
+        for hid in hs:
+            assert np.array_equal(dyn.read_node(hid), ref.read_node(hid)), (t, hid)
+    dyn.close()
+    ref.close()
