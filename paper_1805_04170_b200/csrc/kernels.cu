@@ -422,8 +422,10 @@ __global__ void __launch_bounds__(kThreads, 4) col2im_kernel(const ConvDesc* __r
   const int c = tile / ngrp, gb = tile - c * ngrp;
   const int nb0 = gb * G, Gn = min(G, NB - nb0);
   const T* col0 = reinterpret_cast<const T*>(d.a.ptr) + int64_t(nb0) * img + int64_t(c * U * V) * pitch;
-  T* out0 = reinterpret_cast<T*>(d.out) + (int64_t(nb0) * C + c) * HW;
-  T* dact0 = d.b.ptr ? reinterpret_cast<T*>(d.b.ptr) + (int64_t(nb0) * C + c) * HW : nullptr;
+  // out[nb, c, y, x] at nb*on + c*oc + y*W + x (b.st: dense [n, c] or the channel-major layout)
+  const int64_t on = d.b.st[0] ? d.b.st[0] : int64_t(C) * HW, oc = d.b.st[1] ? d.b.st[1] : HW;
+  T* out0 = reinterpret_cast<T*>(d.out) + int64_t(nb0) * on + int64_t(c) * oc;
+  T* dact0 = d.b.ptr ? reinterpret_cast<T*>(d.b.ptr) + int64_t(nb0) * on + int64_t(c) * oc : nullptr;
   for (int t = threadIdx.x; t < min(UV, 32); t += kThreads) ctoff[t] = t * pitch - (t / V) * Xo - (t % V);
   __syncthreads();
   // item (g, y, x) advanced by kThreads per iteration without divisions
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 4) col2im_kernel(const ConvDesc* __r
         for (int vv = v_lo; vv <= v_hi; ++vv) acc += eld(crow + int64_t(vv) * pitch + (x - vv));
       }
     }
-    const int64_t o = int64_t(g) * C * HW + y * W + x;
+    const int64_t o = int64_t(g) * on + y * W + x;
     est(out0 + o, acc);
     if (dact0) {
       float h = acc;  // the stored value

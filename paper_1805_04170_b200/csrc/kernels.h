@@ -102,7 +102,8 @@ enum ConvModeCode : int {
                          //   pitch >= N*img, 16-byte rows)
   CONV_COL2IM = 5,       // out[n,c,y,x] = sum_{u,v} col[(c*U*V+u*V+v)*pitch + n*img + (y-u)*Xo+(x-v)]
                          //   (a.ptr = col, a.shape[0] = N, p = C,U,V,Yo,Xo,pitch,img; taps in
-                         //   ascending (u, v) order; b.ptr != null: also b[...] = 1 - tanh(out)^2)
+                         //   ascending (u, v) order; b.ptr != null: also b[...] = 1 - tanh(out)^2;
+                         //   b.st[0], b.st[1] = image / channel strides of out and b, 0 = dense)
                          //   p[6..7] = launch geometry, set by conv_prepare
 };
 struct ConvDesc {

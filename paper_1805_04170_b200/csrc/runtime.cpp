@@ -85,6 +85,7 @@ struct Lowerer {
   struct Tail {
     int batch;
     std::vector<std::pair<int, int64_t>> probs;
+    bool like = false;  // fused outputs take the source's (strided) layout
   };
   std::map<int, Tail> chain_tail;
   // grad_input node -> its col2im descriptor (open batch: desc index; emitted: conv batch, desc,
@@ -124,6 +125,34 @@ struct Lowerer {
     int64_t n = 1;
     for (auto e : s) n *= e;
     return contiguous_view(alloc_bytes(size_t(n) * size_t(g_es)), s);
+  }
+  // Fresh storage with v's shape and strides (padding inside the extent stays 0).
+  StridedView alloc_like(const StridedView& v) {
+    int64_t ext = 1;
+    for (int i = 0; i < v.rank; ++i) ext += (v.shape[i] - 1) * v.st[i];
+    StridedView t = v;
+    t.ptr = alloc_bytes(size_t(ext) * size_t(g_es));
+    return t;
+  }
+  // Channel-major conv layout [n, c, y, x] -> element c*ld + n*img + y*X + x: every channel's
+  // images side by side in one row of ld = pitch4(N * img) elements, img = pitch4(Y * X).  The
+  // tensor-core conv lowering keeps activations and gradients in this layout: it is the GEMMs'
+  // column layout, so no permute runs between the convolutions.
+  StridedView conv_layout(int64_t N, int64_t C, int64_t Y, int64_t X) {
+    const int64_t img = pitch4(Y * X), ld = pitch4(N * img);
+    StridedView v;
+    v.rank = 4;
+    v.shape[0] = N; v.shape[1] = C; v.shape[2] = Y; v.shape[3] = X;
+    v.st[0] = img; v.st[1] = ld; v.st[2] = X; v.st[3] = 1;
+    v.ptr = alloc_bytes(size_t(C * ld) * size_t(g_es));
+    return v;
+  }
+  static bool is_conv_layout(const StridedView& v) {
+    if (v.rank != 4) return false;
+    const int64_t img = pitch4(v.shape[2] * v.shape[3]), ld = pitch4(v.shape[0] * img);
+    return (v.shape[0] == 1 || v.st[0] == img) && (v.shape[1] == 1 || v.st[1] == ld) &&
+           (v.shape[2] == 1 || v.st[2] == v.shape[3]) && v.st[3] == 1 &&
+           (reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0;
   }
 
   int rank_of(int dev) const { return P.dev_rank[size_t(dev)]; }
@@ -352,7 +381,10 @@ struct Lowerer {
       o_gemm = int(prog.gemm_specs.size()) - 1;
     }
     o_pre_op = op.id;
-    const StridedView out = alloc(n.region.shape());
+    const Shape osh = n.region.shape();
+    if (osh.size() != 4) fail("op '" + op.id + "': conv output must be rank 4");
+    // forward / grad_input outputs in the channel-major conv layout, grad_weight dense
+    const StridedView out = op.mode == ConvMode::grad_weight ? alloc(osh) : conv_layout(osh[0], osh[1], osh[2], osh[3]);
     set_val(ni, out);
     const StridedView a = value(n.sources[0]);
     const StridedView b = value(n.sources[1]);
@@ -398,24 +430,22 @@ struct Lowerer {
     auto& specs = prog.gemm_specs[size_t(o_gemm)];
     double flops = 0;
     if (op.mode == ConvMode::forward) {
-      // out[n][o][yx] = Kmat[o, cuv] . col[cuv, n*YX + yx]   (one problem per image)
+      // Z[o, (n, yx)] = Kmat[o, cuv] . col[cuv, (n, yx)]: one GEMM over every image's (padded)
+      // columns, written straight into the conv layout (padding columns: col's are 0, so Z's are)
       const int64_t NB = a.shape[0], C = a.shape[1], O = b.shape[0], U = b.shape[2], V = b.shape[3];
       const int64_t Yo = out.shape[2], Xo = out.shape[3], K = C * U * V, YX = Yo * Xo;
       int64_t ld = 0;
       const int64_t img = pitch4(YX);
       float* col = im2col(a, U, V, Yo, Xo, img, ld);
-      const MatView km = filter(b);
-      Tail tail{o_gemm, {}};
-      for (int64_t i = 0; i < NB; ++i) {
-        GemmSpec s;
-        s.a = km;
-        s.b = MatView{eoff(col, i * img), K, YX, ld, 1};  // [K x YX] row-major (MN-major operand)
-        s.c = eoff(out.ptr, i * O * YX);
-        s.c_rs = YX;
-        specs.push_back(s);
-        tail.probs.push_back({int(specs.size()) - 1, i * O * YX});
-      }
-      if (fuse) chain_tail[ni] = tail;  // act(z) runs in these problems' epilogues
+      if (ld != out.st[1]) fail("op '" + op.id + "': conv layout pitch mismatch");
+      GemmSpec s;
+      s.a = filter(b);
+      s.b = MatView{col, K, NB * img, ld, 1};  // [K x (n, yx)] row-major (MN-major operand)
+      s.c = out.ptr;
+      s.c_rs = ld;
+      specs.push_back(s);
+      Tail tail{o_gemm, {{int(specs.size()) - 1, 0}}, true};
+      if (fuse) chain_tail[ni] = tail;  // act(z) runs in the GEMM's epilogue
       flops = 2.0 * double(NB) * double(O) * double(YX) * double(K);
     } else if (op.mode == ConvMode::grad_weight) {
       // gk[o, cuv] = Gp[o, (n,yx)] . col[cuv, (n,yx)]^T
@@ -458,6 +488,8 @@ struct Lowerer {
       d.a.shape[0] = NB;
       d.out = out.ptr;
       d.n = out.elements() / out.shape[3];  // rows (n, c, y)
+      d.b.st[0] = out.st[0];  // image / channel strides of out (and of the fused 1 - tanh^2)
+      d.b.st[1] = out.st[1];
       d.p[0] = C; d.p[1] = U; d.p[2] = V; d.p[3] = Yo; d.p[4] = Xo; d.p[5] = ld; d.p[6] = img;
       o_post.descs.push_back(d);
       if (fuse) post_open[ni] = int(o_post.descs.size()) - 1;
@@ -477,6 +509,7 @@ struct Lowerer {
     }
     auto hit = gp_cache.find(key);
     if (hit != gp_cache.end()) return hit->second;
+    if (is_conv_layout(g) && g.st[1] == ld && (g.shape[0] == 1 || g.st[0] == img)) return g.ptr;  // already Gp
     if (!o_pre.descs.empty() && o_pre_op != op) flush();
     o_pre_op = op;
     const int64_t NB = g.shape[0], O = g.shape[1], Xo = g.shape[3];
@@ -514,7 +547,7 @@ struct Lowerer {
       const PostTail pt = post_tail[n.sources[0]];
       ConvDesc& d = prog.conv[size_t(pt.batch)].descs[size_t(pt.desc)];
       if (d.b.ptr) return false;
-      const StridedView out = alloc(n.region.shape());
+      const StridedView out = alloc_like(value(n.sources[0]));
       set_val(ni, out);
       d.b.ptr = out.ptr;
       post_tail.erase(n.sources[0]);
@@ -556,7 +589,7 @@ struct Lowerer {
       st.o_rs = ov.st[0];
       st.o_cs = ov.shape[1] == 1 ? 1 : ov.st[1];
     }
-    const StridedView out = alloc(n.region.shape());
+    const StridedView out = tail.like ? alloc_like(value(src)) : alloc(n.region.shape());
     set_val(ni, out);
     for (const auto& pp : tail.probs) {
       auto& spec = prog.gemm_specs[size_t(tail.batch)][size_t(pp.first)];
