@@ -462,6 +462,7 @@ struct Lowerer {
       s.c = out.ptr;
       s.c_rs = K;
       specs.push_back(s);
+      if (fuse) chain_tail[ni] = Tail{o_gemm, {{int(specs.size()) - 1, 0}}};  // SGD step + update
       flops = 2.0 * double(O) * double(K) * double(NB * YX);
     } else {
       // dcol[cuv, (n, yx)] = Kmat[o, cuv]^T . Gp[o, (n, yx)]   (one GEMM), then
@@ -564,7 +565,7 @@ struct Lowerer {
     if (j_tail < 0) return false;
     const int src = n.sources[size_t(j_tail)];
     const Tail tail = chain_tail[src];
-    const bool multi = tail.probs.size() > 1 || pl.nodes[size_t(src)].region.shape().size() != 2;  // conv
+    const bool multi = tail.probs.size() > 1 || tail.like;  // per-image problems / conv layout
     for (const auto& pp : tail.probs)
       if (prog.gemm_specs[size_t(tail.batch)][size_t(pp.first)].n_epi >= kMaxEpi) return false;
     const int gstep = gemm_step[size_t(tail.batch)];
@@ -584,10 +585,19 @@ struct Lowerer {
       const int avail = P.avail_step[size_t(other)];
       if (gstep >= 0 && avail >= gstep) return false;
       const StridedView& ov = value(other);
-      if (ov.rank != 2) return false;
-      st.other = ov.ptr;
-      st.o_rs = ov.st[0];
-      st.o_cs = ov.shape[1] == 1 ? 1 : ov.st[1];
+      if (ov.rank == 2) {
+        st.other = ov.ptr;
+        st.o_rs = ov.st[0];
+        st.o_cs = ov.shape[1] == 1 ? 1 : ov.st[1];
+      } else if (ov.rank == 4 && value(src).rank == 4 && value(src).contiguous() && ov.st[3] == 1 &&
+                 ov.st[2] == ov.shape[3] && ov.st[1] == ov.shape[2] * ov.shape[3]) {
+        // a filter [o, c, u, v] as the [o, cuv] matrix of the grad_weight GEMM's output
+        st.other = ov.ptr;
+        st.o_rs = ov.st[0];
+        st.o_cs = 1;
+      } else {
+        return false;
+      }
     }
     const StridedView out = tail.like ? alloc_like(value(src)) : alloc(n.region.shape());
     set_val(ni, out);
