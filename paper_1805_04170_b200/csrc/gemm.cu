@@ -41,6 +41,7 @@ constexpr int BK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
 constexpr int CW = 16;                                    // epilogue chunk: 16 accumulator columns
 constexpr uint32_t kOutStage = 32 * CW * 4;               // one 32-row x CW fp32 box (64B swizzle)
 constexpr uint32_t kOutStageBytes = 8 * kOutStage;        // <= 8 epilogue warps x 1 transpose box
+// (TMA-store epilogues: nbox boxes per warp, one per output of the chain)
 constexpr int kOtherDepth = 4;                            // max operand boxes in flight per warp
 constexpr uint32_t kOtherBox = 8 * kOutStage;             // one box for each of <= 8 epilogue warps
 constexpr uint32_t kSmemMax = 232448;                     // 227 KB opt-in
@@ -54,12 +55,12 @@ __host__ __device__ constexpr uint32_t stage_bytes(int bn, bool split) {
   return operand_bytes(bn) * (split ? 2u : 1u);
 }
 // odepth = operand boxes in flight per epilogue warp (0 = no TMA-staged operand)
-inline int stages_for(int bn, bool split, int odepth) {
-  const uint32_t budget = kSmemMax - 1024 - kBarBytes - kOutStageBytes - odepth * kOtherBox;
+inline int stages_for(int bn, bool split, int odepth, int nbox = 1) {
+  const uint32_t budget = kSmemMax - 1024 - kBarBytes - nbox * kOutStageBytes - odepth * kOtherBox;
   return std::min<int>(8, int(budget / stage_bytes(bn, split)));
 }
-inline size_t smem_for(int bn, bool split, int odepth, int stages) {
-  return size_t(stages) * stage_bytes(bn, split) + kOutStageBytes + odepth * kOtherBox + 1024 + kBarBytes;
+inline size_t smem_for(int bn, bool split, int odepth, int stages, int nbox = 1) {
+  return size_t(stages) * stage_bytes(bn, split) + nbox * kOutStageBytes + odepth * kOtherBox + 1024 + kBarBytes;
 }
 // 12 warps: producer, MMA, TMEM allocator, spare, then 8 epilogue warps (two per TMEM lane
 // quarter, each on half the tile's columns) -- or, for 3xTF32, 4 epilogue + 4 splitting warps.
@@ -377,7 +378,8 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* out_stage = smem + STAGES * STAGE;  // [4 warps][32 rows x 128 B] store transpose
-  uint8_t* other_stage = out_stage + kOutStageBytes;  // [8 warps][depth][32 rows x 64 B] if has_other
+  const int NBOX = max(1, (has_other >> 8) & 7);       // output boxes per epilogue warp
+  uint8_t* other_stage = out_stage + NBOX * kOutStageBytes;  // [8 warps][depth][32 rows x 64 B] if has_other
   const int ODEPTH = (has_other >> 4) & 7;  // operand ring depth (0 when unused)
   uint64_t* full = reinterpret_cast<uint64_t*>(other_stage + ODEPTH * kOtherBox);
   uint64_t* empty = full + STAGES;
@@ -707,7 +709,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       const int oe = pr.other_stage;
       const void* omap = pr.tmap_other;
       const bool o_tma = omap != nullptr;
-      const uint32_t sbuf = smem_u32(out_stage + ew * kOutStage);
+      const uint32_t sbuf = smem_u32(out_stage + ew * NBOX * kOutStage);
       // epilogue descriptors in registers for the whole segment (the chunk loop stores through
       // generic pointers, so the compiler would otherwise re-load them from global per chunk)
       const int nout = 1 + pr.n_epi;
@@ -737,6 +739,91 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
           fast = fast && ocs[e] == 1;
           if (e > 0 && epi_needs_other(eop[e - 1]) && e - 1 != oe) fast = false;
         }
+      if (pr.tstore && (oe < 0 || o_tma)) {
+        // TMA-store epilogue: the lane keeps its accumulator row; each stage's 32 x CW values
+        // go to this warp's smem box for that output and one thread issues the bulk tensor
+        // stores (clipped at the problem edges by the tensor maps).  No transpose, no per-lane
+        // global stores.
+        const uint64_t spol = policy_evict_first();  // outputs far larger than L2 (ostream)
+        const uint32_t box0 = smem_u32(out_stage) + uint32_t(ew * NBOX) * kOutStage;
+#pragma unroll 1
+        for (int c0 = c_begin; c0 < c_end; c0 += CSTEP) {
+          const int q0 = sg.tq * BN + c0;
+          float v[CW], o[CW];
+          if (have) {
+            tmem_ld16(taddr + c0, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) v[j] = 0.f;
+          }
+          if (c0 + CSTEP >= c_end) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tmem_empty_lead + acc * 8);
+          }
+          if (q0 >= QQ) continue;
+          if (sg.kind == SEG_HEAD) {
+            for (int pp = 0; pp < sg.n_parts; ++pp) {
+#pragma unroll
+              for (int j = 0; j < CW / 4; ++j) {
+                const float4 x = __ldcg(ws_ptr(ws, wslot(sg.slot + pp), BN, c0, j, row));
+                v[4 * j] += x.x; v[4 * j + 1] += x.y; v[4 * j + 2] += x.z; v[4 * j + 3] += x.w;
+              }
+            }
+          }
+          if (oe >= 0) {
+            mbar_wait(&other_bar[ew * ODEPTH + o_slot], o_phase);
+            const uint32_t ob = smem_u32(other_stage + (ew * ODEPTH + o_slot) * kOutStage);
+#pragma unroll
+            for (int j = 0; j < CW / 4; ++j) {
+              const float4 x = obox_row<BF16>(ob, lane, j);
+              o[4 * j] = x.x; o[4 * j + 1] = x.y; o[4 * j + 2] = x.z; o[4 * j + 3] = x.w;
+            }
+            if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
+            __syncwarp();
+            if (lane == 0) issue_other();
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) o[j] = 0.f;
+          }
+          // the previous chunk's stores have read the boxes
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll
+          for (int e = 0; e <= kMaxEpi; ++e) {
+            if (e >= nout) break;
+            if (e > 0) epi_apply(eop[e - 1], v, o, esc[e - 1]);
+            const uint32_t bx = box0 + uint32_t(e) * kOutStage;
+            if constexpr (BF16) {
+#pragma unroll
+              for (int j = 0; j < CW / 4; ++j) {
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(v[4 * j], v[4 * j + 1]);
+                const __nv_bfloat162 hi = __floats2bfloat162_rn(v[4 * j + 2], v[4 * j + 3]);
+                asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(bx + lane * (CW * 2) + j * 8),
+                             "r"(*reinterpret_cast<const uint32_t*>(&lo)), "r"(*reinterpret_cast<const uint32_t*>(&hi))
+                             : "memory");
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < CW / 4; ++j) sts128(bx + box_off(lane, j), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+#pragma unroll
+            for (int j = 0; j < CW; ++j) v[j] = rnd<BF16>(v[j]);  // the next stage reads the stored value
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            for (int e = 0; e < nout; ++e) {
+              const uint32_t bx = box0 + uint32_t(e) * kOutStage;
+              if (ostream) tma_store_2d_hint(pr.tmap_out[e], bx, q0, prow0, spol);
+              else asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(pr.tmap_out[e]),
+                                "r"(bx), "r"(q0), "r"(prow0) : "memory");
+            }
+            bulk_commit();
+          }
+        }
+        continue;
+      }
       if (fast) {
         // Per-segment store state: row pointer of row (prow0 + lane/4), column 4*(lane%4), per
         // output, and the 8-row step.  The elementwise chain is matched against the fused
@@ -938,6 +1025,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       }
     }
   }
+  if (warp >= 4 && warp < 4 + NEPI && lane == 0) bulk_wait<0>();  // TMA-store epilogue drained
   tc_fence_before();
   if constexpr (PAIR) cluster_sync();  // both CTAs done with the pair's TMEM and barriers
   else __syncthreads();
@@ -1000,6 +1088,7 @@ const CUtensorMapL2promotion kOtherPromo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, 
                                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
 bool g_no_pair = false;
 int g_max_bn = 0;  // debug: cap the tile width
+bool g_no_tma_out = false;  // debug: per-lane global stores instead of TMA-store epilogues
 bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-in (10,0)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1095,8 +1184,9 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 8) g_no_stream = (sbo == 1);  // (8,1) no L2 streaming hints
   if (lbo == 9) g_max_bn = int(sbo);       // (9,n) tile width <= n
   if (lbo == 10) g_no_dyn = (sbo == 1);    // (10,0) dynamic / (10,1) static whole-tile schedules
+  if (lbo == 11) g_no_tma_out = (sbo == 1);  // (11,1) per-lane global stores in the epilogue
   if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
-  if (lbo >= 1 && lbo <= 10) g_dbg_lbo = g_dbg_sbo = 0;
+  if (lbo >= 1 && lbo <= 11) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1341,6 +1431,26 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
       }
       break;
     }
+    // TMA-store epilogue for a lone row-major, 16-byte-pitched output (measured: faster for
+    // plain products, e.g. the conv grad_input columns; slower than the per-lane stores when a
+    // chain of stages shares the epilogue smem with the operand ring)
+    bool ts = !g_no_tma_out && s.n_epi == 0;
+    for (int e = 0; e <= s.n_epi; ++e) {
+      const float* b = e == 0 ? pr.out : pr.epi[e - 1].out;
+      const long long rs = e == 0 ? pr.out_rs : pr.epi[e - 1].out_rs, cs = e == 0 ? pr.out_cs : pr.epi[e - 1].out_cs;
+      ts = ts && storable(b, rs, cs);
+    }
+    if (ts) {
+      for (int e = 0; e <= s.n_epi; ++e) {
+        const float* b = e == 0 ? pr.out : pr.epi[e - 1].out;
+        const long long rs = e == 0 ? pr.out_rs : pr.epi[e - 1].out_rs;
+        store_maps.emplace_back();
+        make_map(&store_maps.back(), b, pr.Q, pr.P, rs, CW, 32, false, true, bf);
+        store_idx.push_back({int(i), e});
+      }
+      pr.tstore = 1;
+      g.nbox = std::max(g.nbox, 1 + s.n_epi);
+    }
     auto small = [](long long x) { return x >= 0 && x < (1ll << 31); };
     bool ok = small(pr.out_rs) && small(pr.out_cs);
     for (int e = 0; e < s.n_epi; ++e) ok = ok && small(pr.epi[e].out_rs) && small(pr.epi[e].out_cs);
@@ -1415,7 +1525,8 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   for (size_t j = 0; j < store_idx.size(); ++j) {
     GemmProblem& pr = probs[size_t(store_idx[j].first)];
     const void* m = static_cast<CUtensorMap*>(g.d_tmaps) + nload + j;
-    pr.tmap_other = m;
+    if (store_idx[j].second == 1 + kMaxEpi) pr.tmap_other = m;
+    else pr.tmap_out[store_idx[j].second] = m;
   }
   CUDA_CHECK(cudaMalloc(&g.d_problems, probs.size() * sizeof(GemmProblem)));
   CUDA_CHECK(cudaMemcpy(g.d_problems, probs.data(), probs.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
@@ -1427,14 +1538,16 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   // operand ring as deep as possible while the mainloop keeps >= 3 stages (>= 1 box)
   g.odepth = 0;
   if (g.other_smem) {
+    // deepest operand ring that keeps the mainloop's depth (>= 4 stages where possible)
     g.odepth = 1;
+    const int want = std::min(4, stages_for(bn_stage, split, 1, g.nbox));
     for (int d = kOtherDepth; d > 1; --d)
-      if (stages_for(bn_stage, split, d) >= 3) { g.odepth = d; break; }
+      if (stages_for(bn_stage, split, d, g.nbox) >= std::max(3, want)) { g.odepth = d; break; }
   }
-  g.stages = stages_for(bn_stage, split, g.odepth);
+  g.stages = stages_for(bn_stage, split, g.odepth, g.nbox);
   if (g_stages > 0) g.stages = std::min(g.stages, g_stages);
   if (g.stages < 1) throw std::runtime_error("gemm: tile does not fit in shared memory");
-  g.smem_bytes = smem_for(bn_stage, split, g.odepth, g.stages);
+  g.smem_bytes = smem_for(bn_stage, split, g.odepth, g.stages, g.nbox);
   g.prefetch = g_prefetch >= 0 ? g_prefetch : 0;
   g.threads = threads_for(split);
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, split, g.pair, g.bf16);
@@ -1447,7 +1560,7 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair, g.bf16);
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
-  const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0);
+  const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8);
   if (g.pair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * g.sched.grid));

@@ -54,6 +54,10 @@ struct GemmProblem {
   // TMA load map of the first epilogue stage's second operand (same 32 x 32 boxes), or null.
   const void* tmap_other = nullptr;
   int other_stage = -1;         // which epi stage tmap_other feeds
+  // TMA store maps of the outputs (product, then each epi stage's), 32 x 16 boxes; tstore = 1
+  // when every output has one (the epilogue then writes boxes to smem and the TMA stores them)
+  const void* tmap_out[1 + kMaxEpi] = {nullptr, nullptr, nullptr, nullptr};
+  int tstore = 0;
 };
 
 // One unit of a CTA's work list: k-blocks [kb0, kb1) of output tile (tp, tq) of problem `prob`.
@@ -105,6 +109,7 @@ struct GemmLaunch {
   int prefetch = 0;             // k-blocks of L2 prefetch ahead of the ring (0 = off)
   bool other_smem = false;      // epilogue operand staged through TMA
   int odepth = 0;               // its boxes in flight per epilogue warp
+  int nbox = 1;                 // smem output boxes per epilogue warp (TMA-store epilogue)
   GemmSchedule sched;
   void* d_problems = nullptr;   // GemmProblem[nprob] on device
   void* d_tmaps = nullptr;      // 2*nprob CUtensorMap on device
