@@ -469,22 +469,22 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   // bar: local barrier (single CTA); bar_c: the leader's barrier in the cluster window (pair)
   auto load_kblock = [&](const GemmProblem& pr, int kb, int p0, int q0, uint8_t* sa, uint8_t* sb,
                          uint64_t* bar, uint32_t bar_c, uint64_t pol_a, uint64_t pol_b) {
-    const int k0 = kb * BKE;
+    const int ka = kb * BKE, kq = kb * BKE;
     if constexpr (!P_MN) {
-      ld2(sa, pr.tmap_a, bar, bar_c, k0, p0, pol_a);
+      ld2(sa, pr.tmap_a, bar, bar_c, ka, p0, pol_a);
     } else if (pr.a3d) {
-      ld3(sa, pr.tmap_a, bar, bar_c, 0, k0, p0 / MNC, pol_a);
+      ld3(sa, pr.tmap_a, bar, bar_c, 0, ka, p0 / MNC, pol_a);
     } else {
 #pragma unroll
-      for (int j = 0; j < BM / MNC; ++j) ld2(sa + j * MNCH, pr.tmap_a, bar, bar_c, p0 + MNC * j, k0, pol_a);
+      for (int j = 0; j < BM / MNC; ++j) ld2(sa + j * MNCH, pr.tmap_a, bar, bar_c, p0 + MNC * j, ka, pol_a);
     }
     if constexpr (!Q_MN) {
-      ld2(sb, pr.tmap_b, bar, bar_c, k0, q0, pol_b);
+      ld2(sb, pr.tmap_b, bar, bar_c, kq, q0, pol_b);
     } else if (pr.b3d) {
-      ld3(sb, pr.tmap_b, bar, bar_c, 0, k0, q0 / MNC, pol_b);
+      ld3(sb, pr.tmap_b, bar, bar_c, 0, kq, q0 / MNC, pol_b);
     } else {
 #pragma unroll
-      for (int j = 0; j < BNH / MNC; ++j) ld2(sb + j * MNCH, pr.tmap_b, bar, bar_c, q0 + MNC * j, k0, pol_b);
+      for (int j = 0; j < BNH / MNC; ++j) ld2(sb + j * MNCH, pr.tmap_b, bar, bar_c, q0 + MNC * j, kq, pol_b);
     }
   };
   if (warp == 0 && lane == 0) {
@@ -1331,7 +1331,8 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     for (const auto& s : specs) kmax = std::max<long long>(kmax, s.ta ? s.a.rows : s.a.cols);
     const long long kb = (kmax + (s0.bf16 ? 63 : 31)) / (s0.bf16 ? 64 : 32);
     auto tiles = [&](int bn) {
-      const bool pair = !split && !g_no_pair && bn == 256 && (g.swap ? N0 : M0) >= 256 && num_sms >= 4;
+      const long long pe = g.swap ? N0 : M0;
+      const bool pair = !split && !g_no_pair && bn == 256 && pe >= 256 && num_sms >= 4 && (pe % 256 == 0 || pe >= 2048);
       const long long pbm = pair ? 256 : 128;
       long long t = 0;
       for (const auto& s : specs) {
@@ -1354,7 +1355,8 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   g.nprob = int(specs.size());
   // CTA pairs (256 x 256 tiles, half the operand bytes per SM) for wide TF32 problems
   const long long P0 = g.swap ? N0 : M0;
-  g.pair = !split && !g_no_pair && g.bn == 256 && P0 >= 256 && num_sms >= 4;
+  // (a P extent that is not a multiple of 256 would leave half of its last pair tile idle)
+  g.pair = !split && !g_no_pair && g.bn == 256 && P0 >= 256 && num_sms >= 4 && (P0 % 256 == 0 || P0 >= 2048);
   const int pbm = g.pair ? 2 * BM : BM;
   const int bnh = g.pair ? g.bn / 2 : g.bn;  // B columns one CTA stages (its TMA box)
 

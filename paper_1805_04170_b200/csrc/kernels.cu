@@ -352,13 +352,10 @@ __device__ __forceinline__ void im2col_items(const T* __restrict__ base, int is,
 }
 
 template <class T>
-__global__ void __launch_bounds__(kThreads) im2col_kernel(const ConvDesc* __restrict__ ds, int n) {
+__device__ __forceinline__ void im2col_body(const ConvDesc& d, int tile) {
   //   out[(c*U*V + u*V + v)*pitch + nb*img + y*Xo + x] = a[nb, c, y+u, x+v]
   extern __shared__ __align__(16) unsigned char move_smem[];
   __shared__ int toff[kMaxTapChunk];  // tap (u, v) -> source offset
-  const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
-  const ConvDesc& d = ds[di];
-  const int tile = int(int64_t(blockIdx.x) - d.tile_begin);
   const int NB = int(d.a.shape[0]);
   const int U = int(d.p[0]), V = int(d.p[1]), Yo = int(d.p[2]), Xo = int(d.p[3]);
   const int64_t pitch = d.p[4], img = d.p[5];
@@ -465,6 +462,51 @@ __global__ void __launch_bounds__(kThreads, 4) col2im_kernel(const ConvDesc* __r
     if (x >= W) { x -= W; ++y; }
     while (y >= H) { y -= H; ++g; }
   }
+}
+
+template <class T>
+__device__ __forceinline__ void shiftpad_body(const ConvDesc& d, int tile) {
+  // V shifted copies of a [n, o, y, x] view into a channel-major grid (V = 1: a plain layout
+  // change, e.g. the gradient permuted for grad_weight):
+  //   out[v*vst + o*ld + n*Sp + top + y*Wp + x + v] = a[n, o, y, x]
+  // block = (channel o, group of G images); items over the group's flat (image, y, x), read
+  // once (coalesced along x), written V times (coalesced runs).
+  const int NB = int(d.a.shape[0]);
+  const int V = int(d.p[0]), Yo = int(d.p[1]), Xo = int(d.p[2]), G = int(d.p[7]);
+  const int64_t Wp = d.p[3], Sp = d.p[4], vst = d.p[5], ld = d.p[6], top = d.b.st[0];
+  const int YX = Yo * Xo, ngrp = (NB + G - 1) / G;
+  const int o = tile / ngrp, gb = tile - o * ngrp;
+  const int nb0 = gb * G, Gn = min(G, NB - nb0);
+  const T* src = reinterpret_cast<const T*>(d.a.ptr) + int64_t(nb0) * d.a.st[0] + int64_t(o) * d.a.st[1];
+  T* dst = reinterpret_cast<T*>(d.out) + int64_t(o) * ld + int64_t(nb0) * Sp + top;
+  // 4 items in flight per thread: item i = threadIdx.x + k * kThreads
+  for (int it0 = threadIdx.x; it0 < Gn * YX; it0 += 4 * kThreads) {
+    T val[4];
+    int64_t dof[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int it = it0 + j * kThreads;
+      dof[j] = -1;
+      if (it < Gn * YX) {
+        const int g = it / YX, r = it - g * YX, y = r / Xo, x = r - y * Xo;
+        val[j] = src[int64_t(g) * d.a.st[0] + int64_t(y) * d.a.st[2] + int64_t(x) * d.a.st[3]];
+        dof[j] = int64_t(g) * Sp + int64_t(y) * Wp + x;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (dof[j] >= 0)
+        for (int v = 0; v < V; ++v) dst[dof[j] + v * (vst + 1)] = val[j];
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) premove_kernel(const ConvDesc* __restrict__ ds, int n) {
+  const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
+  const ConvDesc& d = ds[di];
+  const int tile = int(int64_t(blockIdx.x) - d.tile_begin);
+  if (d.mode == CONV_IM2COL) im2col_body<T>(d, tile);
+  else shiftpad_body<T>(d, tile);
 }
 
 template <class T>
@@ -637,11 +679,17 @@ void conv_prepare(ConvBatch& b) {
   const int64_t es = b.bf16 ? 2 : 4;
   for (auto& d : b.descs) {
     if ((d.mode >= CONV_IM2COL) != b.move) throw std::runtime_error("conv batch mixes compute and data movement");
-    if (b.move && d.mode != b.descs[0].mode) throw std::runtime_error("conv batch mixes im2col and col2im");
+    if (b.move && (d.mode == CONV_COL2IM) != (b.descs[0].mode == CONV_COL2IM))
+      throw std::runtime_error("conv batch mixes col2im with pre-GEMM movement");
     d.tile_begin = tiles;
     if (b.move) {
       const int64_t NB = std::max<int64_t>(d.a.shape[0], 1);
-      if (d.mode == CONV_IM2COL) {
+      if (d.mode == CONV_SHIFTPAD) {
+        const int64_t YX = std::max<int64_t>(d.p[1] * d.p[2], 1);
+        const int64_t G = std::min(NB, std::max<int64_t>(1, (4 * kThreads + YX - 1) / YX));
+        d.p[7] = G;
+        tiles += d.a.shape[1] * ((NB + G - 1) / G);
+      } else if (d.mode == CONV_IM2COL) {
         // G images per block: ~4 items per thread, planes within the staging buffer
         const int64_t U = d.p[0], V = d.p[1], YX = d.p[2] * d.p[3];
         const int64_t HW = (d.p[2] + U - 1) * (d.p[3] + V - 1), UV = U * V;
@@ -677,10 +725,11 @@ void conv_run(const ConvBatch& b, cudaStream_t s) {
   const int nd = int(b.descs.size());
   const size_t sm = size_t(b.smem);
   const bool col2im = b.move && b.descs[0].mode == CONV_COL2IM;
+
   if (col2im && b.bf16) col2im_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
   else if (col2im) col2im_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
-  else if (b.move && b.bf16) im2col_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, sm, s>>>(ds, nd);
-  else if (b.move) im2col_kernel<float><<<unsigned(b.tiles), kThreads, sm, s>>>(ds, nd);
+  else if (b.move && b.bf16) premove_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, sm, s>>>(ds, nd);
+  else if (b.move) premove_kernel<float><<<unsigned(b.tiles), kThreads, sm, s>>>(ds, nd);
   else if (b.bf16) conv_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
   else conv_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
   CUDA_CHECK(cudaGetLastError());

@@ -100,6 +100,10 @@ enum ConvModeCode : int {
                          //   (d.n = rows (k, n, y); col2im: d.n = rows (n, c, y))
                          //   (p = U,V,Yo,Xo,pitch,img; img >= Yo*Xo per-image column stride,
                          //   pitch >= N*img, 16-byte rows)
+  CONV_SHIFTPAD = 6,     // out[v*p5 + o*p6 + n*p4 + b.st[0] + y*p3 + x + v] = a[n,o,y,x], v < p0
+                         //   (p = V,Yo,Xo,Wp,Sp,vstride,ld): a [n,o,y,x] view copied into a
+                         //   channel-major grid, V column-shifted copies (V = 1: the gradient
+                         //   permuted for grad_weight)
   CONV_COL2IM = 5,       // out[n,c,y,x] = sum_{u,v} col[(c*U*V+u*V+v)*pitch + n*img + (y-u)*Xo+(x-v)]
                          //   (a.ptr = col, a.shape[0] = N, p = C,U,V,Yo,Xo,pitch,img; taps in
                          //   ascending (u, v) order; b.ptr != null: also b[...] = 1 - tanh(out)^2;

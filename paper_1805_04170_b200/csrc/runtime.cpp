@@ -383,11 +383,18 @@ struct Lowerer {
     o_pre_op = op.id;
     const Shape osh = n.region.shape();
     if (osh.size() != 4) fail("op '" + op.id + "': conv output must be rank 4");
-    // forward / grad_input outputs in the channel-major conv layout, grad_weight dense
-    const StridedView out = op.mode == ConvMode::grad_weight ? alloc(osh) : conv_layout(osh[0], osh[1], osh[2], osh[3]);
-    set_val(ni, out);
     const StridedView a = value(n.sources[0]);
     const StridedView b = value(n.sources[1]);
+    // forward / grad_input outputs in the channel-major conv layout, grad_weight dense
+    StridedView out;
+    if (op.mode == ConvMode::forward) {
+      out = conv_layout(osh[0], osh[1], osh[2], osh[3]);
+    } else if (op.mode == ConvMode::grad_weight) {
+      out = alloc(osh);
+    } else {
+      out = conv_layout(osh[0], osh[1], osh[2], osh[3]);
+    }
+    set_val(ni, out);
     if (a.rank != 4 || b.rank != 4) fail("op '" + op.id + "': conv operands must be rank 4");
     // im2col in the columns layout col[(c,u,v)][(n,y,x)], rows padded to 16 bytes
     // img = per-image column stride: Yo*Xo (dense, one GEMM over all images) or padded to 16
@@ -429,6 +436,7 @@ struct Lowerer {
     };
     auto& specs = prog.gemm_specs[size_t(o_gemm)];
     double flops = 0;
+    bool post = false;  // the value is finished by the post class (col2im)
     if (op.mode == ConvMode::forward) {
       // Z[o, (n, yx)] = Kmat[o, cuv] . col[cuv, (n, yx)]: one GEMM over every image's (padded)
       // columns, written straight into the conv layout (padding columns: col's are 0, so Z's are)
@@ -465,14 +473,13 @@ struct Lowerer {
       if (fuse) chain_tail[ni] = Tail{o_gemm, {{int(specs.size()) - 1, 0}}};  // SGD step + update
       flops = 2.0 * double(O) * double(K) * double(NB * YX);
     } else {
-      // dcol[cuv, (n, yx)] = Kmat[o, cuv]^T . Gp[o, (n, yx)]   (one GEMM), then
+      // dcol[cuv, (n, yx)] = Kmat[o, cuv]^T . Gp[o, (n, yx)] (one GEMM), then
       // col2im: h[n,c,y,x] = sum_{u,v} dcol[(c,u,v), n*YX + (y-u)*Xo + (x-v)]
       const int64_t NB = a.shape[0], O = a.shape[1], Yo = a.shape[2], Xo = a.shape[3];
       const int64_t C = b.shape[1], U = b.shape[2], V = b.shape[3], K = C * U * V, YX = Yo * Xo;
       const MatView km = filter(b);
       const int64_t img = pitch4(YX), ld = pitch4(NB * img);
-      // dcol = Kmat^T . Gp: one GEMM over every image's (padded) columns; the padding columns of
-      // Gp are 0, so dcol's are too (col2im never reads them)
+      // the padding columns of Gp are 0, so dcol's are too (col2im never reads them)
       float* gp = permuted_grad(a, img, ld, op.id);
       float* dcol = alloc_bytes(size_t(K * ld) * size_t(g_es));
       GemmSpec s;
@@ -495,9 +502,10 @@ struct Lowerer {
       o_post.descs.push_back(d);
       if (fuse) post_open[ni] = int(o_post.descs.size()) - 1;
       flops = 2.0 * double(NB) * double(YX) * double(K) * double(O);
+      post = true;
     }
     P.gemm_flops += flops;
-    produced(ni, op.mode == ConvMode::grad_input ? C_POST : C_COMPUTE);
+    produced(ni, post ? C_POST : C_COMPUTE);
   }
 
   // G[n, o, y, x] -> Gp[o][(n, img-strided y, x)], rows of `ld` elements (the padding columns
@@ -513,16 +521,16 @@ struct Lowerer {
     if (is_conv_layout(g) && g.st[1] == ld && (g.shape[0] == 1 || g.st[0] == img)) return g.ptr;  // already Gp
     if (!o_pre.descs.empty() && o_pre_op != op) flush();
     o_pre_op = op;
-    const int64_t NB = g.shape[0], O = g.shape[1], Xo = g.shape[3];
+    const int64_t O = g.shape[1], Yo = g.shape[2], Xo = g.shape[3];
     float* gp = alloc_bytes(size_t(O * ld) * size_t(g_es));
     gp_cache[key] = gp;
-    StridedView src = g, dst = g;
-    src.shape[0] = O; src.shape[1] = NB;  // permuted view of G: (o, n, y, x)
-    src.st[0] = g.st[1]; src.st[1] = g.st[0];
-    dst.ptr = gp;
-    dst.shape[0] = O; dst.shape[1] = NB;
-    dst.st[0] = ld; dst.st[1] = img; dst.st[2] = Xo; dst.st[3] = 1;
-    o_pre.descs.push_back(ndesc(NARY_COPY, dst, {src}));
+    ConvDesc d;  // one (unshifted) copy into the channel-major layout (pre-GEMM movement launch)
+    std::memset(&d, 0, sizeof d);
+    d.mode = CONV_SHIFTPAD;
+    d.a = g;
+    d.out = gp;
+    d.p[0] = 1; d.p[1] = Yo; d.p[2] = Xo; d.p[3] = Xo; d.p[4] = img; d.p[5] = 0; d.p[6] = ld;
+    o_prec.descs.push_back(d);
     return gp;
   }
 

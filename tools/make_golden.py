@@ -75,6 +75,9 @@ def graphs() -> dict:
     g["cfg2r_bf16"] = ref.gen_mlp(64, [256] * 6, dtype_bytes=2)
     g["mlp_train_d2_bf16"] = ref.gen_mlp(8, [8] * 3, dtype_bytes=2)
     g["fcr_alexnet_bf16"] = ref.gen_mlp(32, [576, 256, 256, 64], dtype_bytes=2)
+    # wide channels: the implicit-GEMM grad_input (h channels >= 128), 3x3 and 5x5 taps
+    g["wideconv_b2"] = G.conv_net(2, (12, 12), [3, 16, 128, 144], [(3, 3), (3, 3), (5, 5)])
+    g["wideconv_bf16"] = G.conv_net(2, (12, 12), [3, 16, 128, 144], [(3, 3), (3, 3), (5, 5)], dtype_bytes=2)
     g["alexr_conv_bf16"] = G.conv_net(4, (16, 16), [3, 8, 16, 8], [(5, 5), (3, 3), (3, 3)], dtype_bytes=2)
     g["reduce_kat"] = reduce_kat_graph()
     return g
@@ -109,6 +112,9 @@ def cases():
     for k in (1, 2):
         out.append(("alexr_conv_b4", "data", k, 7))
     out.append(("alexr_conv_b4", "model", 2, 7))
+    for mode, k in (("opt", 0), ("data", 1), ("opt", 1)):
+        out.append(("wideconv_b2", mode, k, 7))
+    out.append(("wideconv_bf16", "opt", 0, 7))
     for name, ks in (("cfg1_bf16", (0, 1)), ("cfg2r_bf16", (0, 2)), ("mlp_train_d2_bf16", (1, 2)),
                      ("fcr_alexnet_bf16", (1,)), ("alexr_conv_bf16", (0, 1))):
         for k in ks:
@@ -149,7 +155,10 @@ def main():
     gs = graphs()
     os.makedirs(GOLDEN, exist_ok=True)
     bad = 0
+    only = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else None
     for name, mode, k, seed in cases():
+        if only and name not in only:
+            continue
         stem = os.path.join(GOLDEN, file_stem(name, mode, k, seed))
         plan_text, arrays = make_case(gs[name], name, mode, k, seed)
         if check:
