@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     // ahead through a per-warp ring.  Lane 0 owns the issue cursor; boxes are issued and
     // consumed in the same (segment, chunk) order.
     uint32_t o_slot = 0, o_phase = 0;  // consumer ring position
+    uint32_t box_half = 0;             // TMA-store epilogue: box set of the next chunk
     uint32_t i_slot = 0;               // issuer ring position (lane 0)
     const uint64_t o_policy = policy_evict_first();  // the elementwise operand is read once
     Cursor icur{0, s_begin, false};                   // issue cursor (lane 0)
@@ -745,10 +746,12 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         // stores (clipped at the problem edges by the tensor maps).  No transpose, no per-lane
         // global stores.
         const uint64_t spol = policy_evict_first();  // outputs far larger than L2 (ostream)
-        const uint32_t box0 = smem_u32(out_stage) + uint32_t(ew * NBOX) * kOutStage;
+        const uint32_t box_w = smem_u32(out_stage) + uint32_t(ew * NBOX) * kOutStage;
+        const bool dbl = NBOX >= 2 * nout;  // two box sets: chunk k+1 fills while k's stores read
 #pragma unroll 1
         for (int c0 = c_begin; c0 < c_end; c0 += CSTEP) {
           const int q0 = sg.tq * BN + c0;
+          const uint32_t box0 = box_w + (dbl ? box_half * uint32_t(nout) * kOutStage : 0u);
           float v[CW], o[CW];
           if (have) {
             tmem_ld16(taddr + c0, v);
@@ -786,8 +789,11 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
 #pragma unroll
             for (int j = 0; j < CW; ++j) o[j] = 0.f;
           }
-          // the previous chunk's stores have read the boxes
-          if (lane == 0) bulk_wait_read<0>();
+          // the stores that last used these boxes have read them
+          if (lane == 0) {
+            if (dbl) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
           __syncwarp();
 #pragma unroll
           for (int e = 0; e <= kMaxEpi; ++e) {
@@ -821,6 +827,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             }
             bulk_commit();
           }
+          box_half ^= 1u;
         }
         continue;
       }
@@ -1451,7 +1458,7 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
         store_idx.push_back({int(i), e});
       }
       pr.tstore = 1;
-      g.nbox = std::max(g.nbox, 1 + s.n_epi);
+      g.nbox = std::max(g.nbox, 2 * (1 + s.n_epi));  // double-buffered boxes
     }
     auto small = [](long long x) { return x >= 0 && x < (1ll << 31); };
     bool ok = small(pr.out_rs) && small(pr.out_cs);
