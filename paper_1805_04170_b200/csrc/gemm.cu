@@ -1231,6 +1231,15 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
   int groups = std::max(1, num_sms / G);
   // at least ~8 k-blocks per group so a partial tile amortises its workspace round trip
   groups = int(std::min<long long>(groups, std::max<long long>(1, U / 8)));
+  // A cut tile's head adds every partial of it serially: with few tiles and a long K, cutting
+  // each tile into ~sqrt(k-block bytes / tile bytes * kb) parts balances the parts' operand
+  // reads against the head's partial reads (e.g. a 64 x 27 grad_weight over 61696 columns).
+  {
+    const GemmProblem& p0 = probs[0];
+    const double kblock = 4.0 * 32 * (128 + bn), tile = 4.0 * 128 * bn;
+    const long long per_tile = std::max<long long>(1, (long long)std::ceil(std::sqrt(double(p0.kb_total) * kblock / tile)));
+    groups = int(std::min<long long>(groups, std::max<long long>(1, (long long)cols.size() * per_tile)));
+  }
   if (force_groups > 0) groups = force_groups;
   const int ncols = int(cols.size());
   const bool whole = ncols >= 8 * groups || ncols % groups == 0;

@@ -108,3 +108,12 @@ def test_schedule_random_and_forced():
         _check(nprob, P, Q, K, bn, sms)
     for force in [1, 2, 7, 37]:
         _check(1, 512, 8192, 8192, 256, 148, force)
+
+
+def test_long_k_few_tiles_caps_the_cut():
+    """A 64 x 27 conv grad_weight over 61696 columns (one tile, 1928 k-blocks): the tile is cut
+    into ~sqrt(kb * k-block bytes / tile bytes) ~ 49 parts, not one per SM, so the head's serial
+    sum of partials stays as short as each part's operand reads."""
+    S, work = _check(1, 64, 27, 61696, 32)
+    assert S["stream_k"] and 30 <= S["grid"] <= 64, S["grid"]
+    assert S["nslots"] == S["grid"] - 1
