@@ -6,6 +6,7 @@ the plan's fetch bytes — per op equal to graph_cost(g, a).per_op[op].bytes
 (proj/src/cost.cpp:244-253), per phase equal to simulate_traffic's phase totals
 (proj/src/simulator.cpp:11-49) — on every rank split of the logical devices.
 """
+import collections
 import json
 import os
 import re
@@ -183,3 +184,26 @@ def test_forced_exchange_lowering(stem):
     assert st["rank_fetch_bytes_in"] == P["fetch_bytes_total"]
     if P["fetch_bytes_total"]:
         assert st["n_nccl_groups"] >= 1
+
+
+@pytest.mark.parametrize("stem", [s for s in STEMS if "conv" in s and ".k0." in s], ids=stem_id)
+def test_conv_lowering_structure(stem):
+    """Host-only lowering of conv plans (csrc/runtime.cpp lower_conv_gemm): every conv sub-op is
+    ONE GEMM problem over all images' columns (channel-major layout, no per-image problems),
+    col2im follows each grad_input, and act / seed / step+upd / dact are fused (no elementwise
+    launch left in a single-device conv step)."""
+    text, P, _, _ = load_golden(stem)
+    ex = PlanExecutor(Context.host_only(), text, flags=1)
+    steps = ex.describe()["main"]["steps"]
+    ops = {o["id"]: o for o in P["graph"]["ops"]}
+    conv_subops = collections.Counter(n["op"] for n in P["nodes"]
+                                      if n["kind"] == "sub_op" and ops[n["op"]]["kind"] == "conv")
+    gemm_probs = collections.Counter()
+    for s in steps:
+        if s["kind"] == "gemm" and ops[s["op"]]["kind"] == "conv":
+            gemm_probs[s["op"]] += s["problems"]
+    assert gemm_probs == conv_subops
+    col2im = {s["op"] for s in steps if s.get("what") == "col2im"}
+    assert col2im == {o for o in conv_subops if ops[o]["attrs"]["mode"] == "grad_input"}
+    assert not [s for s in steps if s.get("what") == "elementwise"], "unfused elementwise launch"
+    assert ex.stats()["n_fused_ew"] == sum(1 for o in P["graph"]["ops"] if o["kind"] == "elementwise")
