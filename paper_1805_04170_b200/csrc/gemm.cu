@@ -392,7 +392,10 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   int* seg_q = reinterpret_cast<int*>(tmem_holder + 2);            // [kSegQ]
   uint64_t* seg_full = reinterpret_cast<uint64_t*>(seg_q + kSegQ);  // [kSegQ]
   uint64_t* seg_empty = seg_full + kSegQ;                           // [kSegQ] (leader's)
+  uint64_t* other_empty = seg_empty + kSegQ;                        // [8 warps][depth] (loader mode)
   const bool dyn = (has_other & 128) != 0;
+  // loader mode: warp 3 issues every epilogue warp's operand boxes (the warps only consume)
+  const bool oload = (has_other & 2048) != 0;
 
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;  // 0 = MMA leader of the pair
   const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
@@ -410,7 +413,10 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       mbar_init(&tmem_full[a], 1);
       mbar_init(&tmem_empty[a], PAIR ? 2 * NEPI : NEPI);  // one arrival per epilogue warp (of both CTAs)
     }
-    for (int w = 0; w < 8 * kOtherDepth; ++w) mbar_init(&other_bar[w], 1);
+    for (int w = 0; w < 8 * kOtherDepth; ++w) {
+      mbar_init(&other_bar[w], 1);
+      mbar_init(&other_empty[w], 1);
+    }
     // queue slot consumers: MMA thread, epilogue warps, split warps, and the peer's producer
     // and epilogue warps (remote arrivals)
     const int n_cons = 1 + NEPI + (SPLIT ? 4 : 0) + (PAIR ? 1 + NEPI : 0);
@@ -575,6 +581,36 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       if constexpr (PAIR) mma_commit_pair(&tmem_full[acc], 0x3);
       else mma_commit(&tmem_full[acc]);
     }
+  } else if (warp == 3 && lane == 0 && oload) {
+    // ---------------- operand loader: the epilogue's elementwise operand boxes (w of
+    // w_next = w - wd), per warp in that warp's consumption order, ODEPTH ahead of it
+    const int ODEPTH = (has_other >> 4) & 7;
+    constexpr int CSTEP = NEPI == 8 ? 2 * CW : CW;
+    const uint64_t pol = policy_evict_first();
+    uint32_t ring[8] = {0, 0, 0, 0, 0, 0, 0, 0}, uses[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    Cursor cur{0, s_begin, false};
+    for (;;) {
+      const int si = next_seg(cur, false);
+      if (si < 0) break;
+      const GemmSeg sg = segs[si];
+      const GemmProblem& pr = probs[sg.prob];
+      if (sg.kind == SEG_PART || !pr.tmap_other) continue;
+      const int qb = sg.tq * BN;
+      for (int k = 0; k < BN / CSTEP; ++k) {
+        for (int e = 0; e < NEPI; ++e) {
+          const int c0 = (NEPI == 8 ? (e >> 2) * CW : 0) + k * CSTEP;
+          if (qb + c0 >= pr.Q) continue;
+          const int slot = e * ODEPTH + int(ring[e]);
+          mbar_wait(&other_empty[slot], ((uses[e] / uint32_t(ODEPTH)) & 1u) ^ 1u);
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&other_bar[slot], uint32_t(32 * CW * ES));
+          tma_load_2d_hint(other_stage + slot * kOutStage, pr.tmap_other, &other_bar[slot], qb + c0,
+                           sg.tp * PBM + int(rank) * BM + (e & 3) * 32, pol);
+          ++uses[e];
+          if (++ring[e] == uint32_t(ODEPTH)) ring[e] = 0;
+        }
+      }
+    }
   } else if (SPLIT && warp >= 8) {  // (SPLIT: NEPI == 4, epilogue warps 4..7)
     // ---------------- 3xTF32 split: hi in place, lo into the stage's second half
     const int tid = threadIdx.x - 256;  // 0..127
@@ -650,7 +686,12 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         }
       }
     };
-    if ((has_other & 1) && lane == 0)
+    // a box was consumed (o_slot already advanced): refill it (own issue) or hand it back
+    auto other_done = [&]() {
+      if (oload) mbar_arrive(&other_empty[ew * ODEPTH + int(o_slot == 0 ? ODEPTH - 1 : o_slot - 1)]);
+      else issue_other();
+    };
+    if ((has_other & 1) && lane == 0 && !oload)
       for (int d = 0; d < ODEPTH; ++d) issue_other();
     Cursor cur{0, s_begin, false};
     for (int i = 0;; ++i) {
@@ -784,7 +825,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             }
             if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
             __syncwarp();
-            if (lane == 0) issue_other();
+            if (lane == 0) other_done();
           } else {
 #pragma unroll
             for (int j = 0; j < CW; ++j) o[j] = 0.f;
@@ -899,7 +940,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
           }
           __syncwarp();  // transpose box and operand box free again
-          if (oe >= 0 && lane == 0) issue_other();
+          if (oe >= 0 && lane == 0) other_done();
           const bool full_blk = vec_ok && rows_in && q0 + CW <= QQ;
           const int gq = q0 + c * 4;
           // store stage e's values, then round them as stored (the next stage reads the stored
@@ -986,7 +1027,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             }
             if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
             __syncwarp();
-            if (lane == 0) issue_other();
+            if (lane == 0) other_done();
           } else {
             load_chunk<BF16>(pr.epi[oe].other, pr.epi[oe].o_rs, pr.epi[oe].o_cs, p, q0, PP, QQ, o);
           }
@@ -1095,7 +1136,10 @@ const CUtensorMapL2promotion kOtherPromo[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, 
                                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
 bool g_no_pair = false;
 int g_max_bn = 0;  // debug: cap the tile width
-bool g_no_tma_out = false;  // debug: per-lane global stores instead of TMA-store epilogues
+bool g_no_tma_out = false;
+// A dedicated warp loads the epilogue operand boxes (fp32: bwd_w + update 3 % faster; bf16's
+// small boxes run 25 % slower with the single loader, so bf16 keeps per-warp issue).
+bool g_other_loader = true;  // debug (12,0) off / (12,1) on  // debug: per-lane global stores instead of TMA-store epilogues
 bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-in (10,0)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1192,8 +1236,9 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 9) g_max_bn = int(sbo);       // (9,n) tile width <= n
   if (lbo == 10) g_no_dyn = (sbo == 1);    // (10,0) dynamic / (10,1) static whole-tile schedules
   if (lbo == 11) g_no_tma_out = (sbo == 1);  // (11,1) per-lane global stores in the epilogue
+  if (lbo == 12) g_other_loader = (sbo == 1);  // (12,0/1) operand-loader warp for fp32 epilogues
   if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
-  if (lbo >= 1 && lbo <= 11) g_dbg_lbo = g_dbg_sbo = 0;
+  if (lbo >= 1 && lbo <= 12) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1578,7 +1623,8 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair, g.bf16);
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
-  const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8);
+  const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
+                    (g.other_smem && g_other_loader && !g.bf16 && !g.sched.dynamic ? 2048 : 0);
   if (g.pair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * g.sched.grid));
