@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     }
     for (int w = 0; w < 8 * kOtherDepth; ++w) {
       mbar_init(&other_bar[w], 1);
-      mbar_init(&other_empty[w], 1);
+      mbar_init(&other_empty[w], oload ? 2 : 1);  // loader mode: both warps of a lane quarter
     }
     // queue slot consumers: MMA thread, epilogue warps, split warps, and the peer's producer
     // and epilogue warps (remote arrivals)
@@ -582,12 +582,12 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       else mma_commit(&tmem_full[acc]);
     }
   } else if (warp == 3 && lane == 0 && oload) {
-    // ---------------- operand loader: the epilogue's elementwise operand boxes (w of
-    // w_next = w - wd), per warp in that warp's consumption order, ODEPTH ahead of it
+    // ---------------- operand loader: the epilogue's elementwise operand (w of
+    // w_next = w - wd) as one 32 x 32 box per TMEM lane quarter and 32-column step (the two
+    // warps of the quarter each read their 16 columns), ODEPTH boxes ahead per quarter
     const int ODEPTH = (has_other >> 4) & 7;
-    constexpr int CSTEP = NEPI == 8 ? 2 * CW : CW;
     const uint64_t pol = policy_evict_first();
-    uint32_t ring[8] = {0, 0, 0, 0, 0, 0, 0, 0}, uses[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t ring[4] = {0, 0, 0, 0}, uses[4] = {0, 0, 0, 0};
     Cursor cur{0, s_begin, false};
     for (;;) {
       const int si = next_seg(cur, false);
@@ -596,18 +596,17 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       const GemmProblem& pr = probs[sg.prob];
       if (sg.kind == SEG_PART || !pr.tmap_other) continue;
       const int qb = sg.tq * BN;
-      for (int k = 0; k < BN / CSTEP; ++k) {
-        for (int e = 0; e < NEPI; ++e) {
-          const int c0 = (NEPI == 8 ? (e >> 2) * CW : 0) + k * CSTEP;
-          if (qb + c0 >= pr.Q) continue;
-          const int slot = e * ODEPTH + int(ring[e]);
-          mbar_wait(&other_empty[slot], ((uses[e] / uint32_t(ODEPTH)) & 1u) ^ 1u);
+      for (int c0 = 0; c0 < BN; c0 += 2 * CW) {
+        if (qb + c0 >= pr.Q) break;
+        for (int q = 0; q < 4; ++q) {
+          const int slot = q * ODEPTH + int(ring[q]);
+          mbar_wait(&other_empty[slot], ((uses[q] / uint32_t(ODEPTH)) & 1u) ^ 1u);
           fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&other_bar[slot], uint32_t(32 * CW * ES));
-          tma_load_2d_hint(other_stage + slot * kOutStage, pr.tmap_other, &other_bar[slot], qb + c0,
-                           sg.tp * PBM + int(rank) * BM + (e & 3) * 32, pol);
-          ++uses[e];
-          if (++ring[e] == uint32_t(ODEPTH)) ring[e] = 0;
+          mbar_arrive_expect_tx(&other_bar[slot], uint32_t(32 * 2 * CW * ES));
+          tma_load_2d_hint(other_stage + slot * (2 * kOutStage), pr.tmap_other, &other_bar[slot], qb + c0,
+                           sg.tp * PBM + int(rank) * BM + q * 32, pol);
+          ++uses[q];
+          if (++ring[q] == uint32_t(ODEPTH)) ring[q] = 0;
         }
       }
     }
@@ -686,9 +685,21 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         }
       }
     };
+    // operand ring of this warp: its own 32 x 16 boxes, or (loader mode) its lane quarter's
+    // 32 x 32 boxes shared with the quarter's other warp (128-byte rows, 128-byte swizzle)
+    const int oring = (oload ? lq : ew) * ODEPTH;
+    auto obar = [&](uint32_t sl) { return &other_bar[oring + int(sl)]; };
+    auto obox = [&](uint32_t sl) {
+      return smem_u32(other_stage) + uint32_t(oring + int(sl)) * (oload ? 2 * kOutStage : kOutStage);
+    };
+    // row r, 16-byte group c (columns 4c..4c+3) of this warp's 16 operand columns
+    auto oread = [&](uint32_t ob, int r, int c) -> float4 {
+      if (oload) return lds128(ob + uint32_t(r) * 128u + (uint32_t(((ew >> 2) * 4 + c) ^ (r & 7)) << 4));
+      return obox_so<BF16>(ob, r, c);
+    };
     // a box was consumed (o_slot already advanced): refill it (own issue) or hand it back
     auto other_done = [&]() {
-      if (oload) mbar_arrive(&other_empty[ew * ODEPTH + int(o_slot == 0 ? ODEPTH - 1 : o_slot - 1)]);
+      if (oload) mbar_arrive(&other_empty[oring + int(o_slot == 0 ? ODEPTH - 1 : o_slot - 1)]);
       else issue_other();
     };
     if ((has_other & 1) && lane == 0 && !oload)
@@ -816,11 +827,11 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
             }
           }
           if (oe >= 0) {
-            mbar_wait(&other_bar[ew * ODEPTH + o_slot], o_phase);
-            const uint32_t ob = smem_u32(other_stage + (ew * ODEPTH + o_slot) * kOutStage);
+            mbar_wait(obar(o_slot), o_phase);
+            const uint32_t ob = obox(o_slot);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
-              const float4 x = obox_row<BF16>(ob, lane, j);
+              const float4 x = oread(ob, lane, j);
               o[4 * j] = x.x; o[4 * j + 1] = x.y; o[4 * j + 2] = x.z; o[4 * j + 3] = x.w;
             }
             if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
@@ -933,10 +944,10 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) x[i] = lds128(sbuf + box_off(i * 8 + (lane >> 2), c));
           if (oe >= 0) {
-            mbar_wait(&other_bar[ew * ODEPTH + o_slot], o_phase);
-            const uint32_t ob = smem_u32(other_stage + (ew * ODEPTH + o_slot) * kOutStage);
+            mbar_wait(obar(o_slot), o_phase);
+            const uint32_t ob = obox(o_slot);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) ox[i] = obox_so<BF16>(ob, i * 8 + (lane >> 2), c);
+            for (int i = 0; i < 4; ++i) ox[i] = oread(ob, i * 8 + (lane >> 2), c);
             if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
           }
           __syncwarp();  // transpose box and operand box free again
@@ -1018,11 +1029,11 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         if (oe >= 0 && q0 < QQ) {
           if (o_tma) {
             // the box was requested ODEPTH chunks ahead; read my row, refill the slot
-            mbar_wait(&other_bar[ew * ODEPTH + o_slot], o_phase);
-            const uint32_t ob = smem_u32(other_stage + (ew * ODEPTH + o_slot) * kOutStage);
+            mbar_wait(obar(o_slot), o_phase);
+            const uint32_t ob = obox(o_slot);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
-              const float4 x = obox_row<BF16>(ob, lane, j);
+              const float4 x = oread(ob, lane, j);
               o[4 * j] = x.x; o[4 * j + 1] = x.y; o[4 * j + 2] = x.z; o[4 * j + 3] = x.w;
             }
             if (++o_slot == uint32_t(ODEPTH)) { o_slot = 0; o_phase ^= 1; }
@@ -1426,6 +1437,10 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   std::vector<std::pair<int, int>> store_idx;  // (problem, output index)
   std::vector<GemmProblem>& probs = g.host_problems;
   probs.resize(specs.size());
+  // loader-warp operand boxes (fp32, 8 epilogue warps, static schedules, Q in whole 32-column
+  // boxes so both warps of a lane quarter consume every box)
+  g.oloader = !bf && !split && g_other_loader && g_no_dyn;
+  for (const auto& s : specs) g.oloader = g.oloader && ((g.swap ? (s.ta ? s.a.cols : s.a.rows) : (s.tb ? s.b.rows : s.b.cols)) % 32 == 0);
   for (size_t i = 0; i < specs.size(); ++i) {
     const GemmSpec& s = specs[i];
     if (!gemm_view_ok(s.a, bf) || !gemm_view_ok(s.b, bf))
@@ -1488,7 +1503,10 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
       pr.other_stage = e;
       if (!g_no_tma_store && storable(pr.epi[e].other, pr.epi[e].o_rs, pr.epi[e].o_cs)) {
         store_maps.emplace_back();
-        make_map(&store_maps.back(), pr.epi[e].other, pr.Q, pr.P, pr.epi[e].o_rs, CW, 32, false, true, bf);
+        if (g.oloader)  // 32 x 32 boxes, 128-byte rows (two warps' chunks)
+          make_map(&store_maps.back(), pr.epi[e].other, pr.Q, pr.P, pr.epi[e].o_rs, 2 * CW, 32, false, false, bf);
+        else
+          make_map(&store_maps.back(), pr.epi[e].other, pr.Q, pr.P, pr.epi[e].o_rs, CW, 32, false, true, bf);
         store_idx.push_back({int(i), 1 + kMaxEpi});
         g.other_smem = true;
       }
@@ -1624,7 +1642,7 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
   const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
-                    (g.other_smem && g_other_loader && !g.bf16 && !g.sched.dynamic ? 2048 : 0);
+                    (g.other_smem && g.oloader && !g.sched.dynamic ? 2048 : 0);
   if (g.pair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * g.sched.grid));

@@ -108,6 +108,7 @@ struct GemmLaunch {
   int stages = 0;               // smem ring depth
   int prefetch = 0;             // k-blocks of L2 prefetch ahead of the ring (0 = off)
   bool other_smem = false;      // epilogue operand staged through TMA
+  bool oloader = false;         // ... by the loader warp, one 32 x 32 box per TMEM lane quarter
   int odepth = 0;               // its boxes in flight per epilogue warp
   int nbox = 1;                 // smem output boxes per epilogue warp (TMA-store epilogue)
   GemmSchedule sched;
