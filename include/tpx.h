@@ -162,6 +162,13 @@ int tpx_gemm_timed(const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs,
 int tpx_gemm_schedule(int nprob, int P, int Q, int K, int bn, int num_sms, int force_groups,
                       int* grid, int* nsegs, int* nslots, int* group, int* stream_k,
                       int32_t* segs, int max_segs, int32_t* seg_off, int max_ctas);
+/* The variant the last tpx_gemm / tpx_gemm_timed on this thread launched (for tests that must
+ * cover a specific kernel): fills min(n, 16) of
+ *   bn, pair (cta_group::2 256-row tiles), swap (computed transposed), p_mn, q_mn (MN-major
+ *   operands), oloader (operand-loader warp), other_smem (TMA-staged epilogue operand),
+ *   stream_k, group, tstore (TMA-store epilogue), nbox, odepth, stages, units (CTAs), split
+ *   (3xTF32), bf16. */
+int tpx_gemm_last_launch(int64_t* info, int n);
 /* Debug: override the MN-major UMMA descriptor strides (bytes; 0 = defaults). */
 int tpx_debug_gemm_mn_desc(unsigned lbo, unsigned sbo);
 

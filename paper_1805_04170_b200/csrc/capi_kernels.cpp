@@ -14,6 +14,20 @@ namespace tpx {
 thread_local std::string g_last_error;
 }
 
+namespace {
+// Variant chosen by the last tpx_gemm / tpx_gemm_timed on this thread (tpx_gemm_last_launch).
+thread_local int64_t g_last_launch[16] = {0};
+
+void record_launch(const tpx::GemmLaunch& g) {
+  bool tstore = false;
+  for (const auto& pr : g.host_problems) tstore = tstore || pr.tstore;
+  const int64_t v[16] = {g.bn, g.pair, g.swap, g.p_mn, g.q_mn, g.other_smem && g.oloader && !g.sched.dynamic,
+                         g.other_smem, g.sched.stream_k, g.sched.group, tstore, g.nbox, g.odepth, g.stages,
+                         g.units, g.split, g.bf16};
+  for (int i = 0; i < 16; ++i) g_last_launch[i] = v[i];
+}
+}  // namespace
+
 extern "C" {
 
 __attribute__((visibility("default"))) const char* tpx_last_error(void) {
@@ -55,6 +69,7 @@ __attribute__((visibility("default"))) int tpx_gemm_timed(
     CUDA_CHECK(cudaGetDevice(&dev));
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     tpx::GemmLaunch g = tpx::gemm_prepare({s}, sms, precision == 1);  // 2: bf16 storage (GemmSpec.bf16)
+    record_launch(g);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     try {
@@ -130,6 +145,13 @@ __attribute__((visibility("default"))) int tpx_gemm_schedule(int nprob, int P, i
     }
     if (seg_off && S.grid + 1 <= max_ctas + 1)
       for (int i = 0; i <= S.grid; ++i) seg_off[i] = S.seg_off[size_t(i)];
+  });
+}
+
+__attribute__((visibility("default"))) int tpx_gemm_last_launch(int64_t* info, int n) {
+  return tpx::guard([&] {
+    if (!info || n < 0) tpx::fail("tpx_gemm_last_launch: null buffer");
+    for (int i = 0; i < n && i < 16; ++i) info[i] = g_last_launch[i];
   });
 }
 

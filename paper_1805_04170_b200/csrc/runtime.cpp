@@ -1308,10 +1308,16 @@ std::string describe(const PlanRt& P) {
         s << "],\"ta\":" << (specs.empty() ? 0 : specs[0].ta) << ",\"tb\":" << (specs.empty() ? 0 : specs[0].tb);
         if (size_t(st.idx) < prog.gemm.size()) {
           const GemmLaunch& gl = prog.gemm[size_t(st.idx)];
+          bool tstore = false;
+          for (const auto& pr : gl.host_problems) tstore = tstore || pr.tstore;
           s << ",\"bn\":" << gl.bn << ",\"swap\":" << gl.swap << ",\"pair\":" << gl.pair
             << ",\"flops\":" << gl.flops << ",\"min_bytes\":" << gl.min_bytes << ",\"units\":" << gl.units
             << ",\"stream_k\":" << gl.sched.stream_k << ",\"group\":" << gl.sched.group
-            << ",\"segments\":" << gl.sched.segs.size() << ",\"partial_slots\":" << gl.sched.nslots;
+            << ",\"segments\":" << gl.sched.segs.size() << ",\"partial_slots\":" << gl.sched.nslots
+            << ",\"oloader\":" << (gl.other_smem && gl.oloader && !gl.sched.dynamic ? 1 : 0)
+            << ",\"other_smem\":" << gl.other_smem << ",\"odepth\":" << gl.odepth << ",\"stages\":" << gl.stages
+            << ",\"p_mn\":" << gl.p_mn << ",\"q_mn\":" << gl.q_mn << ",\"split\":" << gl.split
+            << ",\"bf16\":" << gl.bf16 << ",\"tstore\":" << (tstore ? 1 : 0);
         }
       } else if (st.kind == ST_XCHG) {
         const XchgGroup& g = prog.xchg[size_t(st.idx)];

@@ -74,6 +74,7 @@ _SIGS = {
                           P(c_int), P(c_int), P(c_int), P(ctypes.c_int32), c_int,
                           P(ctypes.c_int32), c_int],
     "tpx_debug_gemm_mn_desc": [ctypes.c_uint, ctypes.c_uint],
+    "tpx_gemm_last_launch": [P(c_i64), c_int],
 }
 
 
@@ -138,6 +139,17 @@ def gemm(A, B, ta: bool, tb: bool, C, epi=None, stream=None, precision: int = 0,
                                ops, scales, others, others_rs, outs, outs_rs, int(precision), s,
                                int(warmup), int(iters), ctypes.byref(ms)))
     return ms.value if iters > 0 else None
+
+
+LAUNCH_FIELDS = ("bn", "pair", "swap", "p_mn", "q_mn", "oloader", "other_smem", "stream_k", "group",
+                 "tstore", "nbox", "odepth", "stages", "units", "split", "bf16")
+
+
+def last_launch():
+    """The kernel variant the last gemm() call on this thread launched (tpx_gemm_last_launch)."""
+    buf = (c_i64 * 16)()
+    check(lib().tpx_gemm_last_launch(buf, 16))
+    return dict(zip(LAUNCH_FIELDS, list(buf)))
 
 
 def gemm_schedule(nprob: int, P_: int, Q: int, K: int, bn: int, num_sms: int = 148,
