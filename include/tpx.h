@@ -84,6 +84,13 @@ typedef struct tpx_plan tpx_plan;
 #define TPX_FLAG_DIRECT_CONV 4
 /* Execute the step as one CUDA graph (captured on the first tpx_execute on a stream). */
 #define TPX_FLAG_GRAPH 8
+/* Training loop: tpx_execute runs one step AND carries the weights into the next one.  Every
+ * weight whose w_next holder has the weight's own layout on each device (loop-consistent
+ * tilings: data-parallel plans, the loop-aware optimum) trades storage with it -- the step is
+ * lowered twice and consecutive steps alternate, so that carry costs no copy; the other
+ * weights run the carry program (tpx_carry_weights' conversion) after the step.  Node reads
+ * see the last executed step; tpx_init_inputs restarts the loop. */
+#define TPX_FLAG_LOOP 16
 int tpx_load_plan(tpx_ctx* ctx, const char* plan_json, size_t len, int precision, int flags,
                   tpx_plan** out);
 int tpx_plan_free(tpx_plan* plan);
@@ -156,10 +163,11 @@ int tpx_gemm_timed(const float* a, int64_t a_rows, int64_t a_cols, int64_t a_rs,
                    const int64_t* epi_out_rs, int precision, uint64_t cuda_stream, int warmup,
                    int iters, double* avg_ms);
 /* Host-only: the persistent GEMM's tile schedule for `nprob` problems of P x Q x K (kernel
- * orientation, 128 x bn tiles, 32-deep k-blocks) on `num_sms` SMs.  segs (8 int32 per segment:
+ * orientation, 128 x bn tiles, 32-deep k-blocks) on `num_sms` SMs; max_kb > 0 bounds every
+ * segment to max_kb k-blocks (the 3xTF32 kernels' accumulation chains).  segs (8 int32 per segment:
  * prob, tp, tq, kb0, kb1, kind, slot, n_parts) and seg_off (grid+1) are filled when large
  * enough.  No GPU needed. */
-int tpx_gemm_schedule(int nprob, int P, int Q, int K, int bn, int num_sms, int force_groups,
+int tpx_gemm_schedule(int nprob, int P, int Q, int K, int bn, int num_sms, int force_groups, int max_kb,
                       int* grid, int* nsegs, int* nslots, int* group, int* stream_k,
                       int32_t* segs, int max_segs, int32_t* seg_off, int max_ctas);
 /* The variant the last tpx_gemm / tpx_gemm_timed on this thread launched (for tests that must

@@ -113,7 +113,7 @@ __attribute__((visibility("default"))) int tpx_gemm(
 }
 
 __attribute__((visibility("default"))) int tpx_gemm_schedule(int nprob, int P, int Q, int K, int bn,
-                                                             int num_sms, int force_groups,
+                                                             int num_sms, int force_groups, int max_kb,
                                                              int* grid, int* nsegs, int* nslots,
                                                              int* group, int* stream_k,
                                                              int32_t* segs, int max_segs,
@@ -130,7 +130,7 @@ __attribute__((visibility("default"))) int tpx_gemm_schedule(int nprob, int P, i
       pr.tiles_q = (Q + bn - 1) / bn;
       pr.kb_total = (K + 31) / 32;
     }
-    tpx::GemmSchedule S = tpx::gemm_schedule(probs, bn, num_sms, force_groups);
+    tpx::GemmSchedule S = tpx::gemm_schedule(probs, bn, num_sms, force_groups, max_kb);
     *grid = S.grid;
     *nsegs = int(S.segs.size());
     *nslots = S.nslots;

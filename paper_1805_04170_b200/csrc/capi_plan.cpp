@@ -167,7 +167,7 @@ TPX_API int tpx_node_view(const tpx_plan* plan, const char* node_id, uint64_t* d
     const tpx::PlanRt& P = rt(plan);
     const int n = node_of(P, node_id);
     if (!P.has_val[size_t(n)]) tpx::fail("node " + std::string(node_id) + " has no value on this rank");
-    const tpx::StridedView& v = P.val[size_t(n)];
+    const tpx::StridedView& v = (P.loop() && P.last == 1) ? P.val_b[size_t(n)] : P.val[size_t(n)];
     *dev_ptr = reinterpret_cast<uint64_t>(v.ptr);
     *rank = v.rank;
     for (int i = 0; i < 4; ++i) {
@@ -185,7 +185,7 @@ TPX_API int tpx_set_stream(tpx_plan* plan, uint64_t cuda_stream) {
 }
 
 TPX_API int tpx_execute(tpx_plan* plan) {
-  return tpx::guard([&] { tpx::run_program(rt(plan), rt(plan).main, nullptr); });
+  return tpx::guard([&] { tpx::run_step(rt(plan)); });
 }
 
 TPX_API int tpx_execute_steps(tpx_plan* plan, int64_t begin, int64_t end) {
@@ -205,6 +205,7 @@ TPX_API int tpx_execute_op(tpx_plan* plan, const char* op_id) {
     const std::string op(op_id ? op_id : "");
     P.plan.op(op);  // validates the id
     tpx::run_program(P, P.main, &op);
+    P.last = 0;
   });
 }
 

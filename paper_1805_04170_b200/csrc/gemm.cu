@@ -1151,6 +1151,7 @@ bool g_no_tma_out = false;
 // A dedicated warp loads the epilogue operand boxes (fp32: bwd_w + update 3 % faster; bf16's
 // small boxes run 25 % slower with the single loader, so bf16 keeps per-warp issue).
 bool g_other_loader = true;  // debug (12,0) off / (12,1) on  // debug: per-lane global stores instead of TMA-store epilogues
+int g_split_kb = 16;   // 3xTF32: k-blocks per TMEM accumulation chain (debug (13, n); 0 = unbounded)
 bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-in (10,0)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1249,7 +1250,8 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 11) g_no_tma_out = (sbo == 1);  // (11,1) per-lane global stores in the epilogue
   if (lbo == 12) g_other_loader = (sbo == 1);  // (12,0/1) operand-loader warp for fp32 epilogues
   if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
-  if (lbo >= 1 && lbo <= 12) g_dbg_lbo = g_dbg_sbo = 0;
+  if (lbo == 13) g_split_kb = int(sbo);  // (13,n) 3xTF32 accumulation chain of n k-blocks
+  if (lbo >= 1 && lbo <= 13) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1264,7 +1266,7 @@ bool gemm_view_ok(const MatView& v, bool bf16) {
 // (column, k-block); each group gets a contiguous, equal share of the units (stream-K) or, when
 // there are plenty of columns, a contiguous run of whole columns.
 GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int num_sms,
-                           int force_groups) {
+                           int force_groups, int max_kb) {
   GemmSchedule S;
   if (probs.empty()) return S;
   // group width: the P-tile count of small-M problems whose Q operand is large (streamed)
@@ -1298,13 +1300,36 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
   }
   if (force_groups > 0) groups = force_groups;
   const int ncols = int(cols.size());
-  const bool whole = ncols >= 8 * groups || ncols % groups == 0;
+  // Bounded k-ranges (3xTF32): every tile's k range is cut into chunks of <= max_kb k-blocks,
+  // each accumulated in TMEM on its own and summed in fp32 (round to nearest) by the head, in k
+  // order.  The tensor cores' fp32 accumulation does not round to nearest, so its error grows
+  // with the length of one accumulation chain; bounding the chain keeps the split products
+  // fp32-accurate at any K (K = 8192: 4e-5 -> ~1e-6 normwise).
+  bool chunked = false;
+  for (const auto& c : cols) chunked = chunked || (max_kb > 0 && c.kb > max_kb);
+  const bool whole = !chunked && (ncols >= 8 * groups || ncols % groups == 0);
   if (whole) groups = std::min(groups, ncols);
 
   // pieces[col] = ordered (group, kb0, kb1)
   std::vector<std::vector<SchedPiece>> pieces(static_cast<size_t>(ncols));
   std::vector<std::vector<std::pair<int, int>>> group_pieces(static_cast<size_t>(groups));  // (col, piece idx)
-  if (whole) {
+  if (chunked) {
+    // chunks dealt round-robin over the groups (equal k-work each), then each group's list
+    // reordered partial chunks first: heads only wait for partials, which never wait
+    long long i = 0;
+    for (int c = 0; c < ncols; ++c) {
+      const int kb = cols[size_t(c)].kb, nch = std::max(1, (kb + max_kb - 1) / max_kb);
+      for (int j = 0; j < nch; ++j, ++i) {
+        const int g = int(i % groups);
+        pieces[size_t(c)].push_back({g, int((long long)kb * j / nch), int((long long)kb * (j + 1) / nch)});
+        group_pieces[size_t(g)].push_back({c, j});
+      }
+    }
+    for (auto& gp : group_pieces)
+      std::stable_sort(gp.begin(), gp.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+        return (a.second > 0) > (b.second > 0);
+      });
+  } else if (whole) {
     for (int g = 0; g < groups; ++g) {
       const int c0 = int((long long)ncols * g / groups), c1 = int((long long)ncols * (g + 1) / groups);
       for (int c = c0; c < c1; ++c) {
@@ -1559,7 +1584,7 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
       pr.out_stream = ob > kOutStream && !g_no_stream;
     }
   }
-  g.sched = gemm_schedule(probs, g.bn, g.pair ? num_sms / 2 : num_sms, 0);
+  g.sched = gemm_schedule(probs, g.bn, g.pair ? num_sms / 2 : num_sms, 0, split ? g_split_kb : 0);
   if (!g.sched.stream_k && !g_no_dyn) {
     // Whole tiles only: hand them out in order from a device counter instead of fixed per-CTA
     // lists, so SMs that run ahead (less contention, nearer memory) take more tiles and the

@@ -135,7 +135,9 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
 void gemm_run(const GemmLaunch& g, cudaStream_t stream);
 // The tile scheduler alone (host only; exposed for tests).  force_groups > 0 overrides the
 // group count.
-GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int num_sms, int force_groups);
+// max_kb > 0 bounds every segment's k range (3xTF32 accuracy, see gemm.cu).
+GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int num_sms, int force_groups,
+                           int max_kb = 0);
 void gemm_free(GemmLaunch& g);
 // Debug override of the MN-major descriptor strides (0 = defaults).
 void gemm_debug_mn_desc(unsigned lbo, unsigned sbo);

@@ -4,6 +4,7 @@
 #include <cstring>
 #include <set>
 #include <sstream>
+#include <tuple>
 
 #include "json.h"
 #include "nccl_shim.h"
@@ -234,9 +235,15 @@ struct Lowerer {
     return P.val[size_t(node)];
   }
 
-  void set_val(int node, const StridedView& v) {
-    P.val[size_t(node)] = v;
+  // Loop mode, second program: weight buffers and their w_next holders trade storage
+  // (node -> the partner's value in the first program); the fresh allocation is kept unused so
+  // every other node lands at the same arena offset in both programs.
+  const std::map<int, StridedView>* swap_to = nullptr;
+  const StridedView& set_val(int node, const StridedView& v) {
+    auto it = swap_to ? swap_to->find(node) : std::map<int, StridedView>::const_iterator{};
+    P.val[size_t(node)] = (swap_to && it != swap_to->end()) ? it->second : v;
     P.has_val[size_t(node)] = 1;
+    return P.val[size_t(node)];
   }
 
   void ensure_alloc(int node) {
@@ -273,8 +280,7 @@ struct Lowerer {
         o_gemm = int(prog.gemm_specs.size()) - 1;
       }
     }
-    const StridedView out = alloc(n.region.shape());
-    set_val(ni, out);
+    const StridedView out = set_val(ni, alloc(n.region.shape()));
     if (op.kind == OpKind::matmul) {
       GemmSpec s;
       StridedView a = value(n.sources[0]);
@@ -394,7 +400,7 @@ struct Lowerer {
     } else {
       out = conv_layout(osh[0], osh[1], osh[2], osh[3]);
     }
-    set_val(ni, out);
+    out = set_val(ni, out);
     if (a.rank != 4 || b.rank != 4) fail("op '" + op.id + "': conv operands must be rank 4");
     // im2col in the columns layout col[(c,u,v)][(n,y,x)], rows padded to 16 bytes
     // img = per-image column stride: Yo*Xo (dense, one GEMM over all images) or padded to 16
@@ -556,8 +562,7 @@ struct Lowerer {
       const PostTail pt = post_tail[n.sources[0]];
       ConvDesc& d = prog.conv[size_t(pt.batch)].descs[size_t(pt.desc)];
       if (d.b.ptr) return false;
-      const StridedView out = alloc_like(value(n.sources[0]));
-      set_val(ni, out);
+      const StridedView out = set_val(ni, alloc_like(value(n.sources[0])));
       d.b.ptr = out.ptr;
       post_tail.erase(n.sources[0]);
       P.n_fused++;
@@ -607,8 +612,7 @@ struct Lowerer {
         return false;
       }
     }
-    const StridedView out = tail.like ? alloc_like(value(src)) : alloc(n.region.shape());
-    set_val(ni, out);
+    const StridedView out = set_val(ni, tail.like ? alloc_like(value(src)) : alloc(n.region.shape()));
     for (const auto& pp : tail.probs) {
       auto& spec = prog.gemm_specs[size_t(tail.batch)][size_t(pp.first)];
       EpiStage e = st;
@@ -663,8 +667,7 @@ struct Lowerer {
         const PlanNode& cn = pl.nodes[size_t(cat)];
         copy_into(subview(P.val[size_t(cat)], cn.region, n.region), sv);
       } else {
-        const StridedView d = alloc(n.region.shape());
-        set_val(ni, d);
+        const StridedView d = set_val(ni, alloc(n.region.shape()));
         copy_into(d, sv);
         produced(ni, C_COPY);
       }
@@ -695,8 +698,7 @@ struct Lowerer {
         target = subview(P.val[size_t(cat)], cn.region, n.region);
         direct = target.contiguous();
       } else {
-        target = alloc(n.region.shape());
-        set_val(ni, target);
+        target = set_val(ni, alloc(n.region.shape()));
         direct = true;
       }
       if (direct) {
@@ -732,8 +734,7 @@ struct Lowerer {
       need(s, C_REDUCE);
       ins.push_back(value(s));
     }
-    const StridedView out = alloc(n.region.shape());
-    set_val(ni, out);
+    const StridedView out = set_val(ni, alloc(n.region.shape()));
     // Sum in source order (execgraph.cpp:264-282 fixes that order).  More than 8 partials
     // (k > 3) continue as out = out + next 7 in a following launch.
     size_t i = std::min(ins.size(), size_t(kMaxIn));
@@ -754,8 +755,7 @@ struct Lowerer {
   void lower_buffer(int ni) {
     const PlanNode& n = pl.nodes[size_t(ni)];
     if (!mine_dev(n.device)) return;
-    const StridedView v = alloc(n.region.shape());
-    set_val(ni, v);
+    const StridedView v = set_val(ni, alloc(n.region.shape()));
     P.avail_step[size_t(ni)] = -1;
     InitDesc d;
     std::memset(&d, 0, sizeof d);
@@ -829,13 +829,15 @@ struct Lowerer {
     flush();
   }
 
-  // Loop carry: every "<w>_next" holder block onto the holder blocks of weight "<w>".
+  // Loop carry: every "<w>_next" holder block onto the holder blocks of weight "<w>" (weights
+  // carried by the loop-mode swap excepted).
   void run_carry() {
     for (const auto& kv : pl.tensors) {
       const std::string& id = kv.first;
       if (id.size() <= 5 || id.compare(id.size() - 5, 5, "_next") != 0) continue;
       const std::string base = id.substr(0, id.size() - 5);
       if (!pl.tensors.count(base)) continue;
+      if (std::find(P.swapped.begin(), P.swapped.end(), base) != P.swapped.end()) continue;
       if (pl.tensors.at(base).shape != kv.second.shape) continue;
       const auto& src_h = pl.holders.at(id);
       const auto& dst_h = pl.holders.at(base);
@@ -925,9 +927,48 @@ struct Lowerer {
   }
 };
 
+// Loop mode: weights whose buffer on every device of this rank can trade storage with the
+// w_next holder of the same region (an owned allocation of identical layout).
+std::map<int, StridedView> swap_pairs(PlanRt& P) {
+  std::map<int, StridedView> ov;
+  P.swapped.clear();
+  const Plan& pl = P.plan;
+  for (const auto& kv : pl.tensors) {
+    const std::string& id = kv.first;
+    if (id.size() <= 5 || id.compare(id.size() - 5, 5, "_next") != 0) continue;
+    const std::string base = id.substr(0, id.size() - 5);
+    if (!pl.tensors.count(base) || pl.tensors.at(base).shape != kv.second.shape) continue;
+    const auto& wh = pl.holders.at(base);
+    const auto& nh = pl.holders.at(id);
+    std::map<int, StridedView> pairs;
+    bool ok = true;
+    for (int d = 0; d < pl.devices && ok; ++d) {
+      if (P.dev_rank[size_t(d)] != P.ctx->rank) continue;
+      const int b = wh[size_t(d)], h = nh[size_t(d)];
+      const PlanNode& bn = pl.nodes[size_t(b)];
+      const PlanNode& hn = pl.nodes[size_t(h)];
+      ok = bn.kind == NodeKind::buffer &&
+           (hn.kind == NodeKind::sub_op || hn.kind == NodeKind::concat || hn.kind == NodeKind::reduce_partial) &&
+           bn.region.b == hn.region.b && P.has_val[size_t(b)] && P.has_val[size_t(h)];
+      if (!ok) break;
+      const StridedView& vb = P.val[size_t(b)];
+      const StridedView& vh = P.val[size_t(h)];
+      ok = vb.rank == vh.rank && vb.ptr != vh.ptr;
+      for (int i = 0; ok && i < vb.rank; ++i) ok = vb.shape[i] == vh.shape[i] && vb.st[i] == vh.st[i];
+      pairs[b] = vh;
+      pairs[h] = vb;
+    }
+    if (!ok) continue;
+    ov.insert(pairs.begin(), pairs.end());
+    P.swapped.push_back(base);
+  }
+  return ov;
+}
+
 void lower(PlanRt& P, bool dry) {
   g_es = P.esize;
   P.main = Program{};
+  P.main_b = Program{};
   P.carry = Program{};
   P.init = InitBatch{};
   P.val.assign(P.plan.nodes.size(), StridedView{});
@@ -944,6 +985,41 @@ void lower(PlanRt& P, bool dry) {
   {
     Lowerer L(P, P.main, dry);
     L.run_main();
+  }
+  P.swapped.clear();
+  P.val_b.clear();
+  if (P.loop()) {
+    // the same lowering again with the swapped storage: every other allocation repeats at the
+    // same offset, so both programs share one arena; the accounting is the first program's
+    const std::map<int, StridedView> ov = swap_pairs(P);
+    std::vector<StridedView> sv_val;
+    std::vector<char> sv_has;
+    std::vector<int> sv_avail;
+    sv_val.swap(P.val);
+    sv_has.swap(P.has_val);
+    sv_avail.swap(P.avail_step);
+    const size_t used = P.arena_used;
+    const auto acct = std::make_tuple(P.fetch_in, P.xrank_in, P.xrank_out, P.n_fused, P.op_bytes_in, P.phase_bytes_in,
+                                      P.gemm_flops, P.gemm_min_bytes);
+    P.val.assign(P.plan.nodes.size(), StridedView{});
+    P.has_val.assign(P.plan.nodes.size(), 0);
+    P.avail_step.assign(P.plan.nodes.size(), -1);
+    P.arena_used = 0;
+    InitBatch init_a = std::move(P.init);
+    P.init = InitBatch{};
+    {
+      Lowerer L(P, P.main_b, dry);
+      L.swap_to = &ov;
+      L.run_main();
+    }
+    if (P.arena_used != used) fail("loop-mode lowering is not deterministic");
+    P.init = std::move(init_a);  // inputs are seeded where the first program reads them
+    P.val_b.swap(P.val);
+    P.val.swap(sv_val);
+    P.has_val.swap(sv_has);
+    P.avail_step.swap(sv_avail);
+    std::tie(P.fetch_in, P.xrank_in, P.xrank_out, P.n_fused, P.op_bytes_in, P.phase_bytes_in, P.gemm_flops,
+             P.gemm_min_bytes) = acct;
   }
   {
     Lowerer L(P, P.carry, dry);
@@ -979,9 +1055,11 @@ void free_program(Program& prog) {
 
 PlanRt::~PlanRt() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  if (graph_exec_b) cudaGraphExecDestroy(graph_exec_b);
   for (auto& kv : range_graphs) cudaGraphExecDestroy(kv.second);
   free_program(main);
   free_program(carry);
+  free_program(main_b);
   init_free(init);
   for (auto e : events) cudaEventDestroy(e);
   if (io_tmp) cudaFree(io_tmp);
@@ -1034,6 +1112,7 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
     lower(*P, false);
     prepare_program(*P, P->main);
     prepare_program(*P, P->carry);
+    prepare_program(*P, P->main_b);
     P->init.bf16 = P->esize == 2;
     init_prepare(P->init);
   } else {
@@ -1063,12 +1142,15 @@ static void launch_step(PlanRt& P, Program& prog, const Step& s, cudaStream_t st
 void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
   if (P.ctx->host_only()) fail("host-only context cannot execute plans");
   cudaStream_t st = P.stream;
-  if ((P.flags & 8) && !P.timing && !only_op && &prog == &P.main) {
+  const bool is_main = &prog == &P.main || &prog == &P.main_b;
+  if ((P.flags & 8) && !P.timing && !only_op && is_main) {
     // CUDA graph of the whole lowered step (captured on first use, replayed after; the
     // stream must not change in between): one launch instead of one per lowered step
-    if (!P.graph_exec || P.graph_stream != st) {
+    cudaGraphExec_t& ge = &prog == &P.main ? P.graph_exec : P.graph_exec_b;
+    if (!ge || P.graph_stream != st) {
       if (P.graph_exec) cudaGraphExecDestroy(P.graph_exec);
-      P.graph_exec = nullptr;
+      if (P.graph_exec_b) cudaGraphExecDestroy(P.graph_exec_b);
+      P.graph_exec = P.graph_exec_b = nullptr;
       cudaGraph_t g = nullptr;
       CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       try {
@@ -1079,11 +1161,11 @@ void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
         throw;
       }
       CUDA_CHECK(cudaStreamEndCapture(st, &g));
-      CUDA_CHECK(cudaGraphInstantiate(&P.graph_exec, g, 0));
+      CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
       cudaGraphDestroy(g);
       P.graph_stream = st;
     }
-    CUDA_CHECK(cudaGraphLaunch(P.graph_exec, st));
+    CUDA_CHECK(cudaGraphLaunch(ge, st));
     return;
   }
   if (!P.timing || only_op) {
@@ -1117,15 +1199,31 @@ void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
 
 static const StridedView& node_val(PlanRt& P, int node, int64_t n);
 
+void run_step(PlanRt& P) {
+  if (!P.loop()) {
+    run_program(P, P.main, nullptr);
+    P.last = 0;
+    return;
+  }
+  const int par = P.parity;
+  run_program(P, par ? P.main_b : P.main, nullptr);
+  if (!P.carry.steps.empty()) run_program(P, P.carry, nullptr);
+  P.last = par;
+  P.parity ^= 1;
+}
+
 void run_steps(PlanRt& P, int64_t begin, int64_t end) {
   if (P.ctx->host_only()) fail("host-only context cannot execute plans");
-  Program& prog = P.main;
+  // loop mode: the range runs on the program of the current step; the step ends (and the next
+  // one uses the other program, after the carry) with the range that reaches the last step
+  const int par = P.loop() ? P.parity : 0;
+  Program& prog = par ? P.main_b : P.main;
   const int64_t n = int64_t(prog.steps.size());
   if (begin < 0 || end > n || begin > end) fail("step range [" + std::to_string(begin) + ", " + std::to_string(end) +
                                                ") outside the program's " + std::to_string(n) + " steps");
   cudaStream_t st = P.stream;
   if (P.flags & 8) {
-    auto key = std::make_pair(begin, end);
+    auto key = std::make_pair(begin + (int64_t(par) << 40), end);
     auto it = P.range_graphs.find(key);
     if (it == P.range_graphs.end() || P.graph_stream != st) {
       if (P.graph_stream != st) {
@@ -1149,9 +1247,14 @@ void run_steps(PlanRt& P, int64_t begin, int64_t end) {
       it = P.range_graphs.emplace(key, ge).first;
     }
     CUDA_CHECK(cudaGraphLaunch(it->second, st));
-    return;
+  } else {
+    for (int64_t i = begin; i < end; ++i) launch_step(P, prog, prog.steps[size_t(i)], st);
   }
-  for (int64_t i = begin; i < end; ++i) launch_step(P, prog, prog.steps[size_t(i)], st);
+  if (end == n && P.loop()) {
+    if (!P.carry.steps.empty()) run_program(P, P.carry, nullptr);
+    P.last = par;
+    P.parity ^= 1;
+  }
 }
 
 void copy_node_device(PlanRt& P, int node, void* dev, int64_t n, bool to_node) {
@@ -1174,6 +1277,7 @@ void copy_node_device(PlanRt& P, int node, void* dev, int64_t n, bool to_node) {
 
 void init_inputs(PlanRt& P, uint64_t seed) {
   if (P.ctx->host_only()) fail("host-only context cannot execute plans");
+  P.parity = P.last = 0;  // the inputs are seeded where the first program reads them
   if (P.init.descs.empty()) return;
   // re-key the descriptors with the seed (state0 = seed ^ fnv1a(id), dense.cpp:51)
   std::vector<uint64_t> keys;
@@ -1195,7 +1299,7 @@ static const StridedView& node_val(PlanRt& P, int node, int64_t n) {
   if (P.ctx->host_only()) fail("host-only context holds no values");
   if (!P.has_val[size_t(node)])
     fail("node " + P.plan.nodes[size_t(node)].id + " has no value on this rank");
-  const StridedView& v = P.val[size_t(node)];
+  const StridedView& v = (P.loop() && P.last == 1) ? P.val_b[size_t(node)] : P.val[size_t(node)];
   if (v.elements() != n)
     fail("buffer has " + std::to_string(n) + " elements, node " + P.plan.nodes[size_t(node)].id +
          " holds " + std::to_string(v.elements()));
@@ -1358,7 +1462,9 @@ std::string describe(const PlanRt& P) {
   };
   o << ",\"per_op_fetch_bytes_in\":" << map_json(P.op_bytes_in)
     << ",\"per_phase_fetch_bytes_in\":" << map_json(P.phase_bytes_in) << ",\"main\":" << prog_json(P.main)
-    << ",\"carry\":" << prog_json(P.carry) << "}";
+    << ",\"carry\":" << prog_json(P.carry) << ",\"loop\":" << (P.loop() ? 1 : 0) << ",\"swapped\":[";
+  for (size_t i = 0; i < P.swapped.size(); ++i) o << (i ? "," : "") << json_quote(P.swapped[i]);
+  o << "]}";
   return o.str();
 }
 

@@ -83,6 +83,16 @@ struct PlanRt {
   uintptr_t base = 0;
   // programs
   Program main, carry;
+  // TPX_FLAG_LOOP: a second lowering of the step in which every loop-consistent weight's
+  // buffers and its w_next holders trade storage, so consecutive steps alternate main / main_b
+  // and the weights carry over with no copy (the loop carry of the paper's repeated training
+  // step).  Weights whose w_next is tiled differently keep the carry program.
+  Program main_b;
+  std::vector<StridedView> val_b;        // node values as main_b leaves them
+  std::vector<std::string> swapped;      // weight tensors carried by the swap
+  int parity = 0;                        // program of the next step (0 main, 1 main_b)
+  int last = 0;                          // program whose values the node reads see
+  bool loop() const { return (flags & 16) != 0; }
   InitBatch init;
   // accounting
   int64_t fetch_in = 0, xrank_in = 0, xrank_out = 0, carry_bytes = 0, carry_xrank = 0;
@@ -98,7 +108,7 @@ struct PlanRt {
   size_t io_tmp_elems = 0;
   cudaStream_t stream = nullptr;
   // TPX_FLAG_GRAPH: the main program captured as one CUDA graph
-  cudaGraphExec_t graph_exec = nullptr;
+  cudaGraphExec_t graph_exec = nullptr, graph_exec_b = nullptr;
   cudaStream_t graph_stream = nullptr;
   std::map<std::pair<int64_t, int64_t>, cudaGraphExec_t> range_graphs;  // run_steps ranges
 
@@ -108,6 +118,9 @@ struct PlanRt {
 
 PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags);
 void run_program(PlanRt& p, Program& prog, const std::string* only_op);
+// One train step: main (or, in loop mode, main / main_b alternately), then the carry program
+// when the plan has weights the swap cannot carry (loop mode only).
+void run_step(PlanRt& p);
 // Steps [begin, end) of the main program (CUDA graph per range with TPX_FLAG_GRAPH).
 void run_steps(PlanRt& p, int64_t begin, int64_t end);
 // Device-to-device copy between a node's holder block and contiguous device memory (n

@@ -30,6 +30,7 @@ FLAG_FUSE = 1
 FLAG_FORCE_XCHG = 2
 FLAG_DIRECT_CONV = 4  # convolutions as direct CUDA-core loops (cross-check of the tcgen05 lowering)
 FLAG_GRAPH = 8        # the whole step replayed as one CUDA graph
+FLAG_LOOP = 16        # execute() = one training-loop step: the weights carry into the next step
 
 
 @dataclass

@@ -70,7 +70,7 @@ _SIGS = {
     "tpx_gemm_timed": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_int, c_vp,
                        c_i64, c_int, P(c_int), P(ctypes.c_float), P(c_vp), P(c_i64), P(c_vp),
                        P(c_i64), c_int, c_u64, c_int, c_int, P(c_dbl)],
-    "tpx_gemm_schedule": [c_int, c_int, c_int, c_int, c_int, c_int, c_int, P(c_int), P(c_int),
+    "tpx_gemm_schedule": [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, P(c_int), P(c_int),
                           P(c_int), P(c_int), P(c_int), P(ctypes.c_int32), c_int,
                           P(ctypes.c_int32), c_int],
     "tpx_debug_gemm_mn_desc": [ctypes.c_uint, ctypes.c_uint],
@@ -153,17 +153,17 @@ def last_launch():
 
 
 def gemm_schedule(nprob: int, P_: int, Q: int, K: int, bn: int, num_sms: int = 148,
-                  force_groups: int = 0):
+                  force_groups: int = 0, max_kb: int = 0):
     """Host-only view of the persistent GEMM's tile schedule (gemm.cu gemm_schedule):
     returns dict(grid, group, stream_k, nslots, segs=[(prob,tp,tq,kb0,kb1,kind,slot,n_parts)],
     seg_off=[...])."""
     grid, nsegs, nslots, group, sk = (c_int(), c_int(), c_int(), c_int(), c_int())
-    check(lib().tpx_gemm_schedule(nprob, P_, Q, K, bn, num_sms, force_groups, ctypes.byref(grid),
+    check(lib().tpx_gemm_schedule(nprob, P_, Q, K, bn, num_sms, force_groups, max_kb, ctypes.byref(grid),
                                   ctypes.byref(nsegs), ctypes.byref(nslots), ctypes.byref(group),
                                   ctypes.byref(sk), None, 0, None, 0))
     segs = (ctypes.c_int32 * (8 * max(nsegs.value, 1)))()
     off = (ctypes.c_int32 * (grid.value + 1))()
-    check(lib().tpx_gemm_schedule(nprob, P_, Q, K, bn, num_sms, force_groups, ctypes.byref(grid),
+    check(lib().tpx_gemm_schedule(nprob, P_, Q, K, bn, num_sms, force_groups, max_kb, ctypes.byref(grid),
                                   ctypes.byref(nsegs), ctypes.byref(nslots), ctypes.byref(group),
                                   ctypes.byref(sk), segs, nsegs.value, off, grid.value))
     return {"grid": grid.value, "group": group.value, "stream_k": bool(sk.value),

@@ -20,8 +20,8 @@ from paper_1805_04170_b200 import native
 WHOLE, HEAD, PART = 0, 1, 2
 
 
-def _check(nprob, P, Q, K, bn, sms=148, force=0):
-    S = native.gemm_schedule(nprob, P, Q, K, bn, sms, force)
+def _check(nprob, P, Q, K, bn, sms=148, force=0, max_kb=0):
+    S = native.gemm_schedule(nprob, P, Q, K, bn, sms, force, max_kb)
     tiles_p, tiles_q, kbt = -(-P // 128), -(-Q // bn), -(-K // 32)
     assert 1 <= S["grid"] <= max(sms, force)
     segs, off = S["segs"], S["seg_off"]
@@ -33,6 +33,8 @@ def _check(nprob, P, Q, K, bn, sms=148, force=0):
             prob, tp, tq, kb0, kb1, kind, slot, nparts = segs[i]
             assert 0 <= prob < nprob and 0 <= tp < tiles_p and 0 <= tq < tiles_q
             assert 0 <= kb0 <= kb1 <= kbt
+            if max_kb:
+                assert kb1 - kb0 <= max_kb
             by_tile.setdefault((prob, tp, tq), []).append((kb0, kb1, kind, slot, nparts))
             kinds.append(kind)
         # no HEAD before a PART inside one CTA's list
@@ -117,3 +119,17 @@ def test_long_k_few_tiles_caps_the_cut():
     S, work = _check(1, 64, 27, 61696, 32)
     assert S["stream_k"] and 30 <= S["grid"] <= 64, S["grid"]
     assert S["nslots"] == S["grid"] - 1
+
+
+@pytest.mark.parametrize("shape", BASELINE_SHAPES + [(1, 256, 3456, 100352, 256), (1, 128, 27, 61696, 32)])
+@pytest.mark.parametrize("max_kb", [8, 16])
+def test_bounded_chains(shape, max_kb):
+    """3xTF32 schedules: every segment accumulates at most max_kb k-blocks in TMEM (the tensor
+    cores' fp32 accumulation error grows with the chain length); coverage, slot order and the
+    no-head-before-partial rule still hold, and the k-work stays balanced."""
+    S, work = _check(*shape, max_kb=max_kb)
+    kbt = -(-shape[3] // 32)
+    if kbt > max_kb:
+        assert S["stream_k"] and S["nslots"] > 0
+    avg = sum(work) / len(work)
+    assert max(work) <= avg + 2 * max_kb, (max(work), avg)
