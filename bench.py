@@ -1,18 +1,26 @@
 """Benchmark: samples/sec of one SGD train step (forward, backward, update) executed from the
 reference planner's tiling plan on N B200s, optimal tiling vs data parallel.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--precision tf32|fp32]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--precision tf32|fp32|bf16]
                     [--impl ours|reference]
-N > 1 is launched by torchrun (one process per GPU, NCCL); plan k = log2(N), one logical
+N > 1 runs one process per GPU (NCCL): launched by torchrun, or, when WORLD_SIZE is unset, by
+this script re-launching itself under torch.distributed.run.  Plan k = log2(N), one logical
 device per GPU.  Workload (BASELINE.json configs[1]): 5 FC layers, hidden 8192, batch 512
 (`gen_mlp(512, [8192]*6)`), fp32 storage, random-init (seeded_tensor) weights, synthetic
 inputs; plans under plans/ were emitted offline by the unchanged reference planner
-(tools/make_plans.py).  Timed region: K plan executions ("steps"), CUDA events on the
-executor's stream, barrier + synchronize on both sides, max over ranks.  Weights are 1.34 GB
-per step (> 126 MB L2), so no L2 flush is needed between steps.
+(tools/make_plans.py).
+
+A step is one iteration of the training loop: forward, backward, SGD update, and the carry of
+w_next into the next step's w (TPX_FLAG_LOOP: zero-copy when the plan tiles w and w_next alike,
+the carry conversion otherwise).  Timed region: K steps, CUDA events on the executor's stream,
+barrier + synchronize on both sides, max over ranks.  Weights are 1.34 GB per step (> 126 MB
+L2), so no L2 flush is needed between steps.
 
 Rank 0 prints ONE JSON line.  `value` = optimal-tiling plan; `dp` = the data-parallel plan
-(preset_assignment(data)) run by the same kernels in the same process.
+(preset_assignment(data)) run by the same kernels in the same process.  At N = 1 the two are
+the same plan (k = 0), so `variants.tiled_one_gpu` also runs k = 1..3 tiled plans on the one
+GPU (the paper's tiled-on-one-GPU experiment): optimal (+ its carry), data,
+and the loop-aware optimum.
 """
 from __future__ import annotations
 
@@ -109,30 +117,56 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled during the timed region: NVML every 2 ms (pynvml),
+    or nvidia-smi every 50 ms where NVML is unavailable."""
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index, self.rows, self._stop = index, [], threading.Event()
         self._t = None
+        self.source = "nvml"
 
-    def _run(self):
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        while not self._stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((float(sm), float(mx), [n for n, b in zip(self.NAMES, bits) if r & b]))
+            self._stop.wait(0.002)
+
+    def _run_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                r = [x.strip() for x in out.split(",")]
+                if len(r) == 6 and r[0].replace(".", "").isdigit():
+                    self.rows.append((float(r[0]), float(r[1]) if r[1].replace(".", "").isdigit() else None,
+                                      [n for n, v in zip(self.NAMES, r[2:]) if "Active" in v and "Not" not in v]))
             except Exception:  # noqa: BLE001
                 return
             self._stop.wait(0.05)
 
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._run_nvml(nv)
+        except Exception:  # noqa: BLE001
+            self.source = "nvidia-smi"
+            self._run_smi()
+
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.005)
         return self
 
     def __exit__(self, *a):
@@ -142,30 +176,44 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return None
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[2 + i]
-                          and "Not" not in r[2 + i]})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.rows[0][1],
+                "reasons": sorted({n for r in self.rows for n in r[2]}), "samples": len(self.rows),
+                "source": self.source}
 
 
-def cpu_pools(workload, threads):
+def cpu_samples(workload, k, threads):
     """The reference's CPU tiled executor (execute_numeric's node loop through the reference
-    library compiled from its own sources, oracle/_ref) on a bounded sample of each component:
-    ONE sample through ONE layer (a train step of that layer), `threads` independent copies
-    (the reference is single-threaded).  Per component, ratio = the component's per-sample
-    FLOPs / the layer sample's FLOPs; a sample of the workload costs sum(secs x ratio)."""
+    library compiled from its own sources, oracle/_ref) on each component's bounded sample
+    (BASELINE.md §2): the same structure -- layer count, filter sizes, FULL batch -- at reduced
+    widths, planned by the unchanged planner at the same k (plans/<c>.cpusample.*,
+    tools/make_plans.py).  Returns [(component, pool, FLOP ratio full : sample)]."""
     from oracle import ref
     out = []
     for p in parts_of(workload):
-        cfg = CONFIGS[p]
-        text = load_plan(cfg["sample"], "opt", 0)
-        full = graph_flops(json.loads(load_plan(p, "opt", 0))["graph"]) / cfg["batch"]
+        text = load_plan(p + ".cpusample", "opt", k)
+        full = graph_flops(json.loads(load_plan(p, "opt", 0))["graph"])
         ratio = full / graph_flops(json.loads(text)["graph"])
         out.append((p, ref.Pool(text, SEED, threads), ratio))
     return out
+
+
+def cpu_rate(pools, runs, copies):
+    """samples/s of the full workload: per run, each component's sample step (all copies
+    concurrently) scaled by its FLOP ratio; the workload's batch per summed extrapolated time."""
+    per = []
+    for _ in range(runs):
+        per.append(sum(pool.step() * ratio for _, pool, ratio in pools))
+    return copies * len(per) / sum(per), per
+
+
+def cpu_sample_text(workload, pools, copies, extra=""):
+    return (f"{copies} concurrent cop{'y' if copies == 1 else 'ies'} of the reference's tiled node loop "
+            f"(execute_numeric semantics, oracle/_ref built from the reference's sources, fp64, "
+            f"single-threaded each) on reduced-extent graphs of the same structure at full batch "
+            f"({', '.join(f'{p}: FLOP ratio full/sample {r:.4g}' for p, _, r in pools)}); samples/s "
+            f"EXTRAPOLATED to full size by the FLOP ratio (the narrow samples run faster per FLOP than "
+            f"the full widths: cache-resident operands, so the extrapolation favours the reference)" + extra)
 
 
 def run_reference(args):
@@ -174,30 +222,22 @@ def run_reference(args):
         return
     import psutil
     cores = os.cpu_count() or 1
-    widths = [CONFIGS[p]["dims"][1] if "dims" in CONFIGS[p] else 4096 for p in parts_of(args.config)]
-    per_run = 6 * 2 ** 30 * (max(widths) / 8192) ** 2
-    threads = max(1, min(cores, int(psutil.virtual_memory().available * 0.5 // per_run), 64))
-    pools = cpu_pools(args.config, threads)
-    thr = threads
-    for _, pool, _ in pools:  # CPU path: one untimed pass warms caches/allocator
-        if args.warmup:
-            pool.step()
-    per_sample = []  # seconds of one workload sample, per step
-    for _ in range(args.steps):
-        per_sample.append(sum(pool.step() * ratio for _, pool, ratio in pools) / thr)
+    k = int(round(math.log2(max(args.gpus, 1))))
+    threads = max(1, min(cores, int(psutil.virtual_memory().available * 0.5 // (2 << 30)), 128))
+    pools = cpu_samples(args.config, k, threads)
+    for _, pool, _ in pools:  # one untimed pass warms caches / the allocator
+        pool.step()
+    v, per = cpu_rate(pools, max(1, args.steps), threads)
+    v *= workload_batch(args.config)
     for _, pool, _ in pools:
         pool.close()
-    v = len(per_sample) / sum(per_sample)
-    sample = (f"{thr} concurrent copies of the reference's tiled node loop (execute_numeric semantics, "
-              f"fp64, single-threaded each) on one sample through one layer of each component "
-              f"({', '.join(f'{p} x{r:.3g}' for p, _, r in pools)}: FLOP ratio full sample : layer sample) per "
-              f"step; samples/s = copies / sum(layer-sample wall x ratio); 1 warm-up pass")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args.config, int(round(math.log2(max(args.gpus, 1))))),
-        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": thr, "kind": "reference",
-                         "sample": sample},
+        "data": "synthetic", "config": workload_config(args.config, k),
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "reference",
+                         "sample": cpu_sample_text(args.config, pools, threads,
+                                                   f"; {len(per)} steps, each one sample step per copy")},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -285,6 +325,33 @@ def timed(fn, stream, steps, barrier):
     return a.elapsed_time(b)
 
 
+def relaunch(args):
+    """--gpus N > 1 without a torchrun environment: one process per GPU through
+    torch.distributed.run on this node (rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def plan_exists(name, mode, k):
+    return os.path.exists(os.path.join(PLANS, f"{name}.{mode}.k{k}.plan.json.gz"))
+
+
+def parity_summary():
+    """The committed full-size parity results this code was gated by (tests/test_gpu_fullsize.py
+    writes them; profiles/ holds the copy from the last GPU run): reported, not recomputed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_parity_fullsize.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -292,7 +359,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2_mlp5x8192_b512", choices=sorted(CONFIGS) + sorted(NETWORKS))
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32", "bf16"])
-    ap.add_argument("--no-variants", action="store_true", help="skip the bf16 variant beside a tf32 run")
+    ap.add_argument("--no-variants", action="store_true", help="skip the bf16 / fp32 / tiled variants")
     ap.add_argument("--no-graph", action="store_true", help="launch the lowered steps one by one")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -300,10 +367,12 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch(args))
 
     import torch
     import torch.distributed as dist
-    from paper_1805_04170_b200.executor import FLAG_FUSE, FLAG_GRAPH, Context, PlanExecutor
+    from paper_1805_04170_b200.executor import FLAG_FUSE, FLAG_GRAPH, FLAG_LOOP, Context, PlanExecutor
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -313,6 +382,8 @@ def main():
     k = int(round(math.log2(world)))
     if 1 << k != world or k > 3:
         raise SystemExit("N must be 1, 2, 4 or 8")
+    if torch.cuda.device_count() < world and world > 1 and local >= torch.cuda.device_count():
+        raise SystemExit(f"--gpus {world} needs {world} GPUs; this node has {torch.cuda.device_count()}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -334,21 +405,54 @@ def main():
     ctx = Context(local, rank, world)
     if world > 1:
         ctx.init_comm_from_torch()
+        print(f"[bench] rank {rank}: NCCL communicator initialised (nranks={world}, device cuda:{local})",
+              file=sys.stderr, flush=True)
     stream = torch.cuda.Stream()
     hbm_peak, bf16_peak, peak_kind = peaks()
-    res = {}
-    def measure(mode, suffix, prec):
-        """One plan set (every component of the workload) timed end to end."""
+    base_flags = FLAG_FUSE | FLAG_LOOP | (0 if args.no_graph else FLAG_GRAPH)
+
+    def load(mode, suffix, kk, prec, flags):
         exs, texts = [], []
         for part in parts:
-            text = load_plan(part + suffix, mode, k)
-            ex = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE | (0 if args.no_graph else FLAG_GRAPH))
+            text = load_plan(part + suffix, mode, kk)
+            ex = PlanExecutor(ctx, text, precision=prec, flags=flags)
             ex.set_stream(stream.cuda_stream)
             ex.init_inputs(SEED)
             exs.append(ex)
             texts.append(text)
+        return exs, texts
+
+    def stats_of(exs):
         sts = [ex.stats() for ex in exs]
         st = {key: sum(x[key] for x in sts) for key in sts[0]}
+        d = [ex.describe() for ex in exs]
+        st["carry_bytes"] = sum(x["carry_bytes"] for x in d)
+        st["carry_launches"] = sum(len(x["carry"]["steps"]) for x in d)
+        st["swapped"] = sum(len(x["swapped"]) for x in d)
+        return st
+
+    def quick(mode, suffix, kk, prec, flags, steps):
+        """A plan set timed alone (variants): warm-up, then `steps` loop steps."""
+        exs, _ = load(mode, suffix, kk, prec, flags)
+        try:
+            def step():
+                for ex in exs:
+                    ex.execute()
+            for _ in range(args.warmup):
+                step()
+            ms = max_over_ranks(timed(step, stream, steps, barrier))
+            st = stats_of(exs)
+        finally:
+            for ex in exs:
+                ex.close()
+        return {"value": batch * steps / (ms / 1e3), "ms_per_step": ms / steps,
+                "fetch_bytes_total": st["fetch_bytes_total"], "carry_bytes_per_step": st["carry_bytes"],
+                "launches_per_step": st["n_kernel_launches"] + st["carry_launches"]}
+
+    def measure(mode, suffix, prec):
+        """One plan set (every component of the workload) timed end to end."""
+        exs, texts = load(mode, suffix, k, prec, base_flags)
+        st = stats_of(exs)
 
         def step():
             for ex in exs:
@@ -366,11 +470,13 @@ def main():
         g_ms, t_ms, per_step, desc = [], [], [], []
         for ex, part in zip(exs, parts):
             ex.enable_timing(True)
+            ex.init_inputs(SEED)  # restart the loop: the timing pass runs the first program
             desc += [dict(d, part=part if len(parts) > 1 else "") for d in ex.describe()["main"]["steps"]]
         for _ in range(5):
             g = t = 0.0
             ps = []
             for ex in exs:
+                ex.init_inputs(SEED)
                 ex.execute()
                 tt = ex.last_timing()
                 g += tt["gemm_ms"]
@@ -381,6 +487,7 @@ def main():
             per_step.append(ps)
         for ex in exs:
             ex.enable_timing(False)
+            ex.init_inputs(SEED)
         r["gemm_ms"] = statistics.median(g_ms)
         r["timed_total_ms"] = statistics.median(t_ms)
         r["step_ms"] = [statistics.median(x) for x in zip(*per_step)]
@@ -428,6 +535,7 @@ def main():
         nsteps = [len(ex.describe()["main"]["steps"]) for ex in exs]
         copy = torch.cuda.Stream()
         in_ready = torch.cuda.Event()
+        out_read = torch.cuda.Event()  # the previous step's D2H has read the output staging
 
         def stage_inputs():  # next batch: pinned host -> device staging, on the copy stream
             with torch.cuda.stream(copy):
@@ -446,6 +554,8 @@ def main():
             for ex, sp, ns in zip(exs, splits, nsteps):
                 ex.execute_steps(0, sp)
                 outs = [(h, hv, dv) for e2, h, hv, dv in hout if e2 is ex]
+                if outs:
+                    stream.wait_event(out_read)  # no overwrite of dv before its D2H has read it
                 for h, _, dv in outs:
                     ex.copy_node_device(h, dv.data_ptr(), dv.numel(), False)
                 if outs:
@@ -455,6 +565,7 @@ def main():
                     with torch.cuda.stream(copy):
                         for _, hv, dv in outs:
                             hv.copy_(dv, non_blocking=True)
+                    out_read.record(copy)
                 ex.execute_steps(sp, ns)
 
         def e2e_run():
@@ -462,6 +573,7 @@ def main():
                 e2e_step()
             stream.wait_stream(copy)  # the last step's output has reached the host
 
+        out_read.record(copy)
         stage_inputs()
         for _ in range(2):
             e2e_step()
@@ -480,37 +592,71 @@ def main():
             ex.close()
         return r
 
+    res = {}
     suffix = "_bf16" if args.precision == "bf16" else ""
     for mode in ("opt", "data"):
         res[mode] = measure(mode, suffix, prec)
-    # the bf16-storage variant of the optimal plan, reported beside the TF32 headline
     variants = {}
-    if args.precision == "tf32" and not args.no_variants:
-        try:
-            vb = measure("opt", "_bf16", 0)
-            variants["bf16"] = {"value": vb["value"], "ms_per_step": vb["ms_per_step"], "e2e": vb["e2e"],
-                                "dtype": "bf16", "plan": f"kcuts optimal k={k}, graph dtype_bytes 2",
-                                "gemm_ms_per_step": vb["gemm_ms"]}
-        except FileNotFoundError:
-            pass
+    if not args.no_variants:
+        vsteps = max(5, min(args.steps, 20))
+        # the other storage / arithmetic modes of the same plan
+        others = [("bf16", "_bf16", 0)] if args.precision != "bf16" else []
+        if args.precision != "fp32":
+            others.append(("fp32_3xtf32", "", 1))
+        for name, sfx, pv in others:
+            if all(plan_exists(p + sfx, "opt", k) for p in parts):
+                variants[name] = dict(quick("opt", sfx, k, pv, base_flags, vsteps),
+                                      plan=f"kcuts optimal k={k}" + (", graph dtype_bytes 2" if sfx else ""))
+        if world == 1:
+            # tiled on one GPU: 2^kk logical devices share the GPU, fetches are HBM copies
+            free = torch.cuda.mem_get_info()[0]
+            tiled = {}
+            for kk in (1, 2, 3):
+                row = {}
+                for label, mode, flags in (("opt", "opt", base_flags), ("opt_step_only", "opt", base_flags & ~FLAG_LOOP),
+                                           ("data", "data", base_flags), ("loop", "loop", base_flags)):
+                    if not all(plan_exists(p + suffix, mode, kk) for p in parts):
+                        continue
+                    probe = [PlanExecutor(Context.host_only(), load_plan(p + suffix, mode, kk)) for p in parts]
+                    need = sum(x.stats()["device_bytes"] for x in probe)
+                    if need > 0.85 * free:
+                        row[label] = {"skipped": f"arena {need / 2**30:.1f} GiB > 85% of free HBM"}
+                        continue
+                    row[label] = quick(mode, suffix, kk, prec, flags, vsteps)
+                if "data" in row and "value" in row["data"]:
+                    for lab in ("opt", "opt_step_only", "loop"):
+                        if "value" in row.get(lab, {}):
+                            row[f"{lab}_vs_dp"] = row[lab]["value"] / row["data"]["value"]
+                tiled[f"k{kk}"] = row
+            variants["tiled_one_gpu"] = tiled
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            pools = cpu_pools(args.config, 1)
-            secs = sum(pool.step() * ratio for _, pool, ratio in pools)
+            pools = cpu_samples(args.config, 0, 1)
+            for _, pool, _ in pools:
+                pool.step()
+            v, per = cpu_rate(pools, 3, 1)
             for _, pool, _ in pools:
                 pool.close()
-            cpu = {"value": 1.0 / secs, "unit": "samples/s", "cores": 1, "kind": "reference",
-                   "sample": (f"reference tiled node loop (execute_numeric semantics; oracle/_ref built from "
-                              f"the reference's sources; fp64, 1 thread) on 1 sample through 1 layer of each "
-                              f"component of {args.config}, scaled by the FLOP ratio full sample : layer sample "
-                              f"({', '.join(f'{p} x{r:.3g}' for p, _, r in pools)}): {secs:.2f} s per sample")}
+            cpu = {"value": v * batch, "unit": "samples/s", "cores": 1, "kind": "reference",
+                   "sample": cpu_sample_text(args.config, pools, 1,
+                                             f"; 3 runs after 1 warm-up, {sum(per):.1f} s extrapolated")}
+            if args.config != "cfg1_mlp3x1024_b64":
+                # configs[0], the reference's own CPU-runnable case, at FULL size in the same run
+                from oracle import ref
+                pool = ref.Pool(load_plan("cfg1_mlp3x1024_b64", "opt", 0), SEED, 1)
+                t = pool.step()
+                pool.close()
+                cpu["cfg1_full_size"] = {"value": 64 / t, "unit": "samples/s", "seconds_per_step": t,
+                                         "sample": "cfg1 (gen_mlp(64, [1024]*4)) full train step, k=0 plan"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
     if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
         return
     o, d = res["opt"], res["data"]
     flops = o["stats"]["gemm_flops"]
@@ -526,11 +672,16 @@ def main():
         "data": "synthetic",
         "config": workload_config(args.config, k),
         "dp": {"value": d["value"], "ms_per_step": d["ms_per_step"], "plan": f"preset data k={k}",
-               "e2e": d["e2e"]["value"], "fetch_bytes_total": d["stats"]["fetch_bytes_total"]},
+               "e2e": d["e2e"]["value"], "fetch_bytes_total": d["stats"]["fetch_bytes_total"],
+               "carry_bytes_per_step": d["stats"]["carry_bytes"]},
         "opt_vs_dp": o["value"] / d["value"],
         "fetch_bytes_total": o["stats"]["fetch_bytes_total"],
+        "carry_bytes_per_step": o["stats"]["carry_bytes"],
+        "loop_carry": (f"{o['stats']['swapped']} weights carried by buffer swap (zero copy), "
+                       f"{o['stats']['carry_bytes']} cross-device bytes of w_next -> w conversion per step "
+                       f"(unpriced by the planner) in {o['stats']['carry_launches']} extra launches"),
         "e2e": o["e2e"],
-        "gpu_launches": int(o["stats"]["n_kernel_launches"] * args.steps),
+        "gpu_launches": int((o["stats"]["n_kernel_launches"] + o["stats"]["carry_launches"]) * args.steps),
         "roofline": {"bound": dom["bound"], "kernel": f"tcgen05 tile GEMM, {dom['class']} ({dom['what']})",
                      "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
                      "frac": dom["achieved"] / dom["peak"], "traffic": traffic,
@@ -543,11 +694,14 @@ def main():
                      "kernels": kernels,
                      "flops_per_step": flops, "gemm_ms_per_step": o["gemm_ms"],
                      "gemm_share_of_step": o["gemm_ms"] / o["timed_total_ms"],
+                     "timing_pass": ("per-launch CUDA events between every lowered step, graph replay off; "
+                                     "shares are of that pass's total"),
                      "step_roofline_ms": step_roofline_ms(kernels),
                      "step_frac": step_roofline_ms(kernels) / o["ms_per_step"]},
         "clocks": o["clocks"],
         "cpu_baseline": cpu,
         "variants": variants,
+        "parity": parity_summary(),
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -1168,7 +1168,7 @@ void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
     CUDA_CHECK(cudaGraphLaunch(ge, st));
     return;
   }
-  if (!P.timing || only_op) {
+  if (!P.timing || only_op || !is_main) {  // per-step timing covers the step's main program
     for (const auto& s : prog.steps)
       if (!only_op || s.op == *only_op) launch_step(P, prog, s, st);
     return;

@@ -37,19 +37,19 @@ CONV_CONFIGS = {
     "vggconv_b64": lambda: G.vgg_conv(64),          # configs[3] conv component
 }
 # Bounded CPU samples of each config for the reference's CPU executor (bench.py cpu_baseline
-# and --impl reference): one sample through one layer (fwd, act, seed, bwd_w, bwd_x, step,
-# upd) of the same width; a full sample is layers x this.
-SAMPLES = {
-    "cfg1_mlp3x1024_b64": ("cfg1_layer_sample_b1", 1, [1024, 1024], 3),
-    "cfg2_mlp5x8192_b512": ("cfg2_layer_sample_b1", 1, [8192, 8192], 5),
-    "alexfc_b128": ("alexfc_layer_sample_b1", 1, [4096, 4096], 3),
-    "vggfc_b64": ("vggfc_layer_sample_b1", 1, [4096, 4096], 3),
-    "cfg5_mlp3x32768_b32": ("cfg5_layer_sample_b1", 1, [32768, 32768], 3),
-}
-# conv samples: one image through the component's heaviest layer (train step of that layer)
-CONV_SAMPLES = {
-    "alexconv_b128": ("alexconv_layer_sample_b1", lambda: G.conv_net(1, (32, 32), [384, 384], [(3, 3)])),
-    "vggconv_b64": ("vggconv_layer_sample_b1", lambda: G.conv_net(1, (11, 11), [512, 512], [(3, 3)])),
+# and --impl reference), as BASELINE.md §2 plans them: the same structure (layer count, filter
+# sizes, FULL batch) at reduced widths, re-planned by the unchanged planner at the same k, one
+# step ~0.5-1 GFLOP; samples/s are extrapolated to full size by the FLOP ratio (labelled).
+# cfg1 (configs[0], the reference's own CPU-runnable case) is timed at full size.
+CPU_SAMPLES = {
+    "cfg1_mlp3x1024_b64": lambda: ref.gen_mlp(64, [1024] * 4),
+    "cfg2_mlp5x8192_b512": lambda: ref.gen_mlp(512, [256] * 6),
+    "alexfc_b128": lambda: ref.gen_mlp(128, [1152, 512, 512, 125]),
+    "vggfc_b64": lambda: ref.gen_mlp(64, [3136, 512, 512, 125]),
+    "cfg5_mlp3x32768_b32": lambda: ref.gen_mlp(32, [1024] * 4),
+    # (channel splits need multiples of 8 at k = 3)
+    "alexconv_b128": lambda: G.conv_net(128, (24, 24), [3, 8, 8, 16, 16, 8], G.ALEXNET_CONV["filters"]),
+    "vggconv_b64": lambda: G.conv_net(64, (29, 29), [3] + [8] * 13, G.VGG_CONV["filters"]),
 }
 
 
@@ -86,12 +86,9 @@ def main():
                       f"fetch_bytes_total {P['fetch_bytes_total']}")
         if bf16:
             continue
-        if name in CONV_SAMPLES:
-            sname, gen = CONV_SAMPLES[name]
-            write(os.path.join(OUT, f"{sname}.opt.k0.plan.json.gz"), ref.plan(gen(), "opt", 0))
-        else:
-            sname, sb, sdims, _ = SAMPLES[name]
-            write(os.path.join(OUT, f"{sname}.opt.k0.plan.json.gz"), ref.plan(ref.gen_mlp(sb, sdims), "opt", 0))
+        g = CPU_SAMPLES[name]()
+        for k in range(4):
+            write(os.path.join(OUT, f"{name}.cpusample.opt.k{k}.plan.json.gz"), ref.plan(g, "opt", k))
 
 
 if __name__ == "__main__":
