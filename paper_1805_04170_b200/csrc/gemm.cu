@@ -69,6 +69,10 @@ __host__ __device__ constexpr int epi_warps(bool split) { return split ? 4 : 8; 
 __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
   return 2 * bn <= 32 ? 32 : 2 * bn <= 64 ? 64 : 2 * bn <= 128 ? 128 : 2 * bn <= 256 ? 256 : 512;
 }
+// 3xTF32: two accumulators + the fp32 sum of a tile's finished accumulation chains
+__host__ __device__ constexpr uint32_t tmem_cols_split(int bn) {
+  return 3 * bn <= 128 ? 128 : 3 * bn <= 256 ? 256 : 512;
+}
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -366,7 +370,8 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   constexpr uint32_t A_BYTES = BM * BK * 4;
   constexpr uint32_t OPB = operand_bytes(BNH);
   constexpr uint32_t STAGE = stage_bytes(BNH, SPLIT);
-  constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
+  static_assert(!SPLIT || 3 * BN <= 512, "3xTF32 tiles keep a third TMEM region for chain sums");
+  constexpr uint32_t TMEM_COLS = SPLIT ? tmem_cols_split(BN) : tmem_cols_for(BN);
   constexpr int NEPI = epi_warps(SPLIT);
   constexpr uint32_t FMT = BF16 ? 1u : 2u;          // A/B format: bf16 (kind::f16) / tf32
   constexpr uint32_t IDESC = (1u << 4)                 // D format f32
@@ -396,6 +401,14 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   const bool dyn = (has_other & 128) != 0;
   // loader mode: warp 3 issues every epilogue warp's operand boxes (the warps only consume)
   const bool oload = (has_other & 2048) != 0;
+  // 3xTF32 accumulation chains: a segment's k range is accumulated in TMEM CHN k-blocks at a
+  // time; each finished chain is added (fp32, round to nearest) into a third TMEM region.  The
+  // tensor cores' accumulator does not round to nearest, so its error grows with the chain.
+  const int CHN = SPLIT ? ((has_other >> 12) & 15) : 0;
+  auto nchains = [&](const GemmSeg& sg) {
+    const int n = sg.kb1 - sg.kb0;
+    return (CHN > 0 && n > CHN) ? (n + CHN - 1) / CHN : 1;
+  };
 
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;  // 0 = MMA leader of the pair
   const int unit = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
@@ -531,17 +544,23 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   } else if (warp == 1 && lane == 0 && rank == 0) {
     // ---------------- MMA issuer (single thread; the pair's leader CTA)
     uint32_t s = 0, ph = 0;  // ring slot and its phase parity
+    uint32_t ai = 0;         // accumulator uses (one per chain)
     Cursor cur{0, s_begin, false};
-    for (int i = 0;; ++i) {
+    for (;;) {
       const int si = next_seg(cur, true);
       if (si < 0) break;
       const GemmSeg sg = segs[si];
       const GemmProblem& pr = probs[sg.prob];
-      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+      const int nch = nchains(sg);
+      for (int ch = 0; ch < nch; ++ch) {
+      const int ck0 = nch > 1 ? sg.kb0 + ch * CHN : sg.kb0;
+      const int ck1 = nch > 1 ? min(sg.kb1, ck0 + CHN) : sg.kb1;
+      const uint32_t acc = ai & 1, aph = (ai >> 1) & 1;
+      ++ai;
       mbar_wait(&tmem_empty[acc], aph ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
-      for (int kb = sg.kb0; kb < sg.kb1; ++kb, (++s == uint32_t(STAGES)) ? (s = 0, ph ^= 1) : 0) {
+      for (int kb = ck0; kb < ck1; ++kb, (++s == uint32_t(STAGES)) ? (s = 0, ph ^= 1) : 0) {
         if constexpr (SPLIT) mbar_wait(&split_done[s], ph);
         else mbar_wait(&full[s], ph);
         tc_fence_after();
@@ -560,7 +579,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
           const uint64_t bd = !Q_MN ? umma_desc(sb + kk * 32, 16, 1024, 2)
                               : BF16 ? umma_desc(sb + kk * 2048, MNCH, 1024, 2)
                                      : umma_desc(sb + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1);
-          const uint32_t accum = (kb > sg.kb0 || kk > 0) ? 1u : 0u;
+          const uint32_t accum = (kb > ck0 || kk > 0) ? 1u : 0u;
           if constexpr (SPLIT) {
             // low parts live OPB bytes after the high parts, in the same (swizzled) layout
             const uint64_t lo = uint64_t((OPB >> 4) & 0x3FFFu);
@@ -580,6 +599,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       }
       if constexpr (PAIR) mma_commit_pair(&tmem_full[acc], 0x3);
       else mma_commit(&tmem_full[acc]);
+      }
     }
   } else if (warp == 3 && lane == 0 && oload) {
     // ---------------- operand loader: the epilogue's elementwise operand (w of
@@ -705,12 +725,51 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     if ((has_other & 1) && lane == 0 && !oload)
       for (int d = 0; d < ODEPTH; ++d) issue_other();
     Cursor cur{0, s_begin, false};
-    for (int i = 0;; ++i) {
+    uint32_t ai = 0;  // accumulator uses (one per chain)
+    const uint32_t tsum = tmem_base + 2 * BN + (uint32_t(lq * 32) << 16);  // 3xTF32 chain sums
+    for (;;) {
       const int si = next_seg(cur, lane == 0);
       if (si < 0) break;
       const GemmSeg sg = segs[si];
       const GemmProblem& pr = probs[sg.prob];
-      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+      const int nch = nchains(sg);
+      if constexpr (SPLIT) {
+        // every chain but the last: drained into the sum region (this warp's lane quarter, all
+        // columns), then the accumulator goes back to the MMA warp
+        for (int ch = 0; ch + 1 < nch; ++ch) {
+          const uint32_t a2 = ai & 1, ap2 = (ai >> 1) & 1;
+          ++ai;
+          mbar_wait(&tmem_full[a2], ap2);
+          tc_fence_after();
+          const uint32_t ta = tmem_base + a2 * BN + (uint32_t(lq * 32) << 16);
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += CW) {
+            float v[CW], w[CW];
+            tmem_ld16(ta + c0, v);
+            if (ch > 0) {
+              tmem_ld16(tsum + c0, w);
+#pragma unroll
+              for (int j = 0; j < CW; ++j) v[j] = w[j] + v[j];
+            }
+            tmem_st16(tsum + c0, v);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tmem_empty_lead + a2 * 8);
+        }
+      }
+      const bool summed = SPLIT && nch > 1;
+      // the last chain's accumulator plus the earlier chains' sum
+      auto add_sum = [&](int c0, float (&v)[CW]) {
+        if (summed) {
+          float w[CW];
+          tmem_ld16(tsum + c0, w);
+#pragma unroll
+          for (int j = 0; j < CW; ++j) v[j] = w[j] + v[j];
+        }
+      };
+      const uint32_t acc = ai & 1, aph = (ai >> 1) & 1;
+      ++ai;
       const bool have = sg.kb1 > sg.kb0;
       const uint32_t taddr = tmem_base + acc * BN + (uint32_t(lq * 32) << 16);
       if (has_other & 2) mbar_wait_sleep(&tmem_full[acc], aph);
@@ -723,6 +782,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
           float v[CW];
           if (have) {
             tmem_ld16(taddr + c0, v);
+            add_sum(c0, v);
           } else {
 #pragma unroll
             for (int j = 0; j < CW; ++j) v[j] = 0.f;
@@ -807,6 +867,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
           float v[CW], o[CW];
           if (have) {
             tmem_ld16(taddr + c0, v);
+            add_sum(c0, v);
           } else {
 #pragma unroll
             for (int j = 0; j < CW; ++j) v[j] = 0.f;
@@ -917,6 +978,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
           float v[CW];
           if (have) {
             tmem_ld16(taddr + c0, v);
+            add_sum(c0, v);
           } else {
 #pragma unroll
             for (int j = 0; j < CW; ++j) v[j] = 0.f;
@@ -1046,6 +1108,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         float v[CW];
         if (have) {
           tmem_ld16(taddr + c0, v);
+          add_sum(c0, v);
         } else {
 #pragma unroll
           for (int j = 0; j < CW; ++j) v[j] = 0.f;
@@ -1126,7 +1189,9 @@ KernelFn kernel_for_t(int bn, bool p_mn, bool q_mn, bool split, bool pair) {
     case 32: return split ? pick<32, S, false, BF16>(p_mn, q_mn) : pick<32, false, false, BF16>(p_mn, q_mn);
     case 64: return split ? pick<64, S, false, BF16>(p_mn, q_mn) : pick<64, false, false, BF16>(p_mn, q_mn);
     case 128: return split ? pick<128, S, false, BF16>(p_mn, q_mn) : pick<128, false, false, BF16>(p_mn, q_mn);
-    case 256: return split ? pick<256, S, false, BF16>(p_mn, q_mn) : pick<256, false, false, BF16>(p_mn, q_mn);
+    case 256:
+      if (split) throw std::runtime_error("gemm: 3xTF32 tiles are at most 128 wide (TMEM chain sums)");
+      return pick<256, false, false, BF16>(p_mn, q_mn);
   }
   throw std::runtime_error("gemm: unsupported tile width " + std::to_string(bn));
 }
@@ -1151,7 +1216,8 @@ bool g_no_tma_out = false;
 // A dedicated warp loads the epilogue operand boxes (fp32: bwd_w + update 3 % faster; bf16's
 // small boxes run 25 % slower with the single loader, so bf16 keeps per-warp issue).
 bool g_other_loader = true;  // debug (12,0) off / (12,1) on  // debug: per-lane global stores instead of TMA-store epilogues
-int g_split_kb = 16;   // 3xTF32: k-blocks per TMEM accumulation chain (debug (13, n); 0 = unbounded)
+int g_split_kb = 0;    // 3xTF32: k-blocks per scheduled segment (debug (13, n); 0 = unbounded)
+int g_split_chain = 2; // 3xTF32: k-blocks per TMEM accumulation chain (debug (14, n); 0 = unbounded)
 bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-in (10,0)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1250,8 +1316,9 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 11) g_no_tma_out = (sbo == 1);  // (11,1) per-lane global stores in the epilogue
   if (lbo == 12) g_other_loader = (sbo == 1);  // (12,0/1) operand-loader warp for fp32 epilogues
   if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
-  if (lbo == 13) g_split_kb = int(sbo);  // (13,n) 3xTF32 accumulation chain of n k-blocks
-  if (lbo >= 1 && lbo <= 13) g_dbg_lbo = g_dbg_sbo = 0;
+  if (lbo == 13) g_split_kb = int(sbo);  // (13,n) 3xTF32 segments of <= n k-blocks (workspace sums)
+  if (lbo == 14) g_split_chain = int(sbo) & 15;  // (14,n) 3xTF32 TMEM chains of n k-blocks
+  if (lbo >= 1 && lbo <= 14) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1420,6 +1487,7 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   const bool q_mn0 = g.swap ? s0.ta : !s0.tb;
   const int min_bn = (s0.bf16 && q_mn0) ? 64 : 32;
   g.bn = std::max(g.bn, min_bn);
+  if (split) g.bn = std::min(g.bn, 128);  // 3xTF32: TMEM holds 2 accumulators + the chain sums
   {
     // Tile width from the tile count: the widest tile that still gives every SM work.  Short-K
     // (epilogue-bound) problems want a tile per CTA; long-K ones are balanced by stream-K and
@@ -1667,7 +1735,7 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
   const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
-                    (g.other_smem && g.oloader && !g.sched.dynamic ? 2048 : 0);
+                    (g.other_smem && g.oloader && !g.sched.dynamic ? 2048 : 0) | (g.split ? (g_split_chain & 15) << 12 : 0);
   if (g.pair) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * g.sched.grid));

@@ -29,6 +29,8 @@ def put(ex, node_id, value):
     t = node_tensor(ex, node_id)
     v = value.to(device="cuda", dtype=torch.float32)
     t.copy_(v.to(t.dtype))
+    # the executor runs on its own stream: the value must land before its next launch reads it
+    torch.cuda.synchronize()
 
 
 def get(ex, node_id):

@@ -10,7 +10,9 @@ buffer swap), and build_execution_graph on it
 moves exactly the priced bytes.
 
     python tools/make_loop_plans.py CONFIG K [K ...]
-writes plans/<config>.loop.k<K>.plan.json.gz and plans/<config>.loop.k<K>.assignment.json
+writes plans/<config>.loop.k<K>.plan.json.gz and plans/<config>.loop.k<K>.assignment.json;
+    python tools/make_loop_plans.py CONFIG K [K ...] --bf16
+writes the bf16 plans of the cached assignments (plans/<config>_bf16.loop.k<K>.plan.json.gz)
 (planning takes minutes: the unrolled graph's BFS levels merge, see SURVEY finding 9).
 """
 import gzip
@@ -22,7 +24,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle import ref  # noqa: E402
-from tools.make_plans import CONFIGS  # noqa: E402
+from tools.make_plans import CONFIGS, CONV_CONFIGS  # noqa: E402
 
 OUT = os.path.join(ROOT, "plans")
 
@@ -66,12 +68,37 @@ def loop_assignment(graph: dict, unrolled_assignment: dict) -> dict:
     return {"k": unrolled_assignment["k"], "tilings": out}
 
 
+def graph_of(name, dtype_bytes=4):
+    if name in CONV_CONFIGS:
+        g = json.loads(CONV_CONFIGS[name]())
+        for t in g["tensors"]:
+            t["dtype_bytes"] = dtype_bytes
+        return g
+    batch, dims = CONFIGS[name] if name in CONFIGS else (8, [8] * 4)
+    return json.loads(ref.gen_mlp(batch, dims, dtype_bytes=dtype_bytes))
+
+
+def write_bf16(name, k):
+    """The bf16 plan of the same loop-aware tiling (the optimizer minimises elements, so the
+    tilings do not depend on dtype_bytes)."""
+    with open(os.path.join(OUT, f"{name}.loop.k{k}.assignment.json")) as f:
+        a = json.load(f)["assignment"]
+    text = ref.plan(json.dumps(graph_of(name, 2)), json.dumps(a), k)
+    with gzip.GzipFile(os.path.join(OUT, f"{name}_bf16.loop.k{k}.plan.json.gz"), "wb", mtime=0) as f:
+        f.write(text.encode())
+    print(f"{name}_bf16 k={k}: fetch_bytes_total {json.loads(text)['fetch_bytes_total']}", flush=True)
+
+
 def main():
     name = sys.argv[1]
-    batch, dims = CONFIGS[name] if name in CONFIGS else (8, [8] * 4)
-    g = json.loads(ref.gen_mlp(batch, dims))
+    ks = [int(a) for a in sys.argv[2:] if not a.startswith("--")]
+    if "--bf16" in sys.argv:
+        for k in ks:
+            write_bf16(name, k)
+        return
+    g = graph_of(name)
     u = unroll2(g)
-    for k in map(int, sys.argv[2:]):
+    for k in ks:
         t0 = time.time()
         kc = ref.kcuts(json.dumps(u), k)
         a = loop_assignment(g, {"k": k, "tilings": kc["tilings"]})
