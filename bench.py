@@ -363,6 +363,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the lowered steps one by one")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--xchg", default="peer", choices=["peer", "nccl"],
+                    help="N > 1 cross-rank fetches: peer pulls over NVLink (CUDA IPC) or NCCL send/recv")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -372,7 +374,8 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_1805_04170_b200.executor import FLAG_FUSE, FLAG_GRAPH, FLAG_LOOP, Context, PlanExecutor
+    from paper_1805_04170_b200.executor import (FLAG_FORCE_XCHG, FLAG_FUSE, FLAG_GRAPH, FLAG_LOOP, FLAG_PEER,
+                                                Context, PlanExecutor)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -403,19 +406,27 @@ def main():
     batch = workload_batch(args.config)
     prec = 1 if args.precision == "fp32" else 0  # bf16: storage type comes from the bf16 plan
     ctx = Context(local, rank, world)
-    if world > 1:
+    peer = world > 1 and args.xchg == "peer"
+    if world > 1 and not peer:
         ctx.init_comm_from_torch()
         print(f"[bench] rank {rank}: NCCL communicator initialised (nranks={world}, device cuda:{local})",
               file=sys.stderr, flush=True)
     stream = torch.cuda.Stream()
     hbm_peak, bf16_peak, peak_kind = peaks()
-    base_flags = FLAG_FUSE | FLAG_LOOP | (0 if args.no_graph else FLAG_GRAPH)
+    base_flags = FLAG_FUSE | FLAG_LOOP | (0 if args.no_graph else FLAG_GRAPH) | (FLAG_PEER if peer else 0)
+    announced = []
 
     def load(mode, suffix, kk, prec, flags):
         exs, texts = [], []
         for part in parts:
             text = load_plan(part + suffix, mode, kk)
             ex = PlanExecutor(ctx, text, precision=prec, flags=flags)
+            if (flags & FLAG_PEER) and world > 1:
+                ex.connect_peers_from_torch()  # every rank maps every other rank's arena (CUDA IPC)
+                if not announced:
+                    announced.append(1)
+                    print(f"[bench] rank {rank}: peer arenas of {world} ranks mapped over NVLink (CUDA IPC), "
+                          f"device cuda:{local}", file=sys.stderr, flush=True)
             ex.set_stream(stream.cuda_stream)
             ex.init_inputs(SEED)
             exs.append(ex)
@@ -614,7 +625,8 @@ def main():
             for kk in (1, 2, 3):
                 row = {}
                 for label, mode, flags in (("opt", "opt", base_flags), ("opt_step_only", "opt", base_flags & ~FLAG_LOOP),
-                                           ("data", "data", base_flags), ("loop", "loop", base_flags)):
+                                           ("data", "data", base_flags), ("loop", "loop", base_flags),
+                                           ("loop_peer_path", "loop", base_flags | FLAG_FORCE_XCHG | FLAG_PEER)):
                     if not all(plan_exists(p + suffix, mode, kk) for p in parts):
                         continue
                     probe = [PlanExecutor(Context.host_only(), load_plan(p + suffix, mode, kk)) for p in parts]
@@ -624,7 +636,7 @@ def main():
                         continue
                     row[label] = quick(mode, suffix, kk, prec, flags, vsteps)
                 if "data" in row and "value" in row["data"]:
-                    for lab in ("opt", "opt_step_only", "loop"):
+                    for lab in ("opt", "opt_step_only", "loop", "loop_peer_path"):
                         if "value" in row.get(lab, {}):
                             row[f"{lab}_vs_dp"] = row[lab]["value"] / row["data"]["value"]
                 tiled[f"k{kk}"] = row
@@ -670,7 +682,9 @@ def main():
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": {"tf32": "tf32", "fp32": "fp32(3xtf32)", "bf16": "bf16"}[args.precision],
         "data": "synthetic",
-        "config": workload_config(args.config, k),
+        "config": dict(workload_config(args.config, k),
+                       exchange=("peer pull over NVLink (CUDA IPC), device-side phase counters" if peer else
+                                 "NCCL send/recv per phase" if world > 1 else "one rank: HBM copies")),
         "dp": {"value": d["value"], "ms_per_step": d["ms_per_step"], "plan": f"preset data k={k}",
                "e2e": d["e2e"]["value"], "fetch_bytes_total": d["stats"]["fetch_bytes_total"],
                "carry_bytes_per_step": d["stats"]["carry_bytes"]},

@@ -16,8 +16,10 @@
  * Process model: one process per GPU.  A plan with 2^k logical devices is executed by `world`
  * ranks; logical device d belongs to rank (d * world) >> k (contiguous blocks).  With world=1
  * a single GPU hosts every logical device (fetches become HBM copies).  Cross-rank fetches
- * are grouped per plan phase into NCCL send/recv groups (the communicator is created from a
- * 128-byte ncclUniqueId the caller distributes, e.g. with torch.distributed).
+ * are either pulled straight out of the owning rank's arena over NVLink (TPX_FLAG_PEER: the
+ * arenas are shared with CUDA IPC; the caller all-gathers the 64-byte handles, e.g. with
+ * torch.distributed) or grouped per plan phase into NCCL send/recv groups (the communicator is
+ * created from a 128-byte ncclUniqueId the caller distributes).
  */
 #ifndef TPX_H_
 #define TPX_H_
@@ -91,8 +93,22 @@ typedef struct tpx_plan tpx_plan;
  * weights run the carry program (tpx_carry_weights' conversion) after the step.  Node reads
  * see the last executed step; tpx_init_inputs restarts the loop. */
 #define TPX_FLAG_LOOP 16
+/* Peer pull: every cross-rank fetch of a phase is ONE launch on the consuming rank that reads
+ * the strided source boxes out of the owner's arena (CUDA IPC mapping over NVLink) and writes
+ * them at their offsets in the consumer (pack, transfer and unpack in one pass; no NCCL).  A
+ * partial consumed only by a reduce_partial is read in place by the reduction, which also runs
+ * the sum's elementwise consumers (SGD step + update).  Ranks order themselves with device-side
+ * counters in their arenas (a signal per phase with pulls, a barrier per step).  With world > 1
+ * the plan runs only after tpx_plan_connect_peers; with world = 1 and TPX_FLAG_FORCE_XCHG every
+ * cross-device fetch takes this path against the rank's own arena. */
+#define TPX_FLAG_PEER 32
 int tpx_load_plan(tpx_ctx* ctx, const char* plan_json, size_t len, int precision, int flags,
                   tpx_plan** out);
+/* TPX_FLAG_PEER, world > 1: this rank's arena as a CUDA IPC handle (64 bytes) ... */
+int tpx_plan_ipc_handle(tpx_plan* plan, void* out, size_t len);
+/* ... and, with every rank's handle in rank order (world * 64 bytes), map the peers' arenas and
+ * finish the load (lowering against the mapped addresses).  Collective: every rank calls it. */
+int tpx_plan_connect_peers(tpx_plan* plan, const void* handles, size_t len);
 int tpx_plan_free(tpx_plan* plan);
 int tpx_plan_stats(const tpx_plan* plan, tpx_stats* out);
 /* Lowered program as JSON (steps, per-phase message tables, byte counts) — host-only. */
@@ -126,6 +142,7 @@ int tpx_execute_op(tpx_plan* plan, const char* op_id);
 /* Loop carry: after a train step, copy each `<w>_next` tensor's holder blocks onto `<w>`'s
  * holder blocks (conversion between their tilings, fetching across devices as needed). */
 int tpx_carry_weights(tpx_plan* plan);
+/* Waits for the plan stream; fails if a peer wait timed out (TPX_PEER_TIMEOUT_S, default 60 s). */
 int tpx_synchronize(tpx_plan* plan);
 
 /* Per-step device timing of the last tpx_execute (events around each step): total ms and

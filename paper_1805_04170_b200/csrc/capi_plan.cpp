@@ -214,7 +214,26 @@ TPX_API int tpx_carry_weights(tpx_plan* plan) {
 }
 
 TPX_API int tpx_synchronize(tpx_plan* plan) {
-  return tpx::guard([&] { CUDA_CHECK(cudaStreamSynchronize(rt(plan).stream)); });
+  return tpx::guard([&] {
+    CUDA_CHECK(cudaStreamSynchronize(rt(plan).stream));
+    tpx::check_peer_error(rt(plan));
+  });
+}
+
+TPX_API int tpx_plan_ipc_handle(tpx_plan* plan, void* out, size_t len) {
+  return tpx::guard([&] {
+    if (!out) tpx::fail("null output buffer");
+    tpx::arena_ipc_handle(rt(plan), out, len);
+  });
+}
+
+TPX_API int tpx_plan_connect_peers(tpx_plan* plan, const void* handles, size_t len) {
+  return tpx::guard([&] {
+    if (!handles) tpx::fail("null handle table");
+    tpx::PlanRt& P = rt(plan);
+    if (!P.ctx->host_only()) CUDA_CHECK(cudaSetDevice(P.ctx->ordinal));
+    tpx::connect_peers(P, handles, len);
+  });
 }
 
 TPX_API int tpx_enable_timing(tpx_plan* plan, int on) {

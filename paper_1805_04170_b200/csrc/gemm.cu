@@ -42,10 +42,10 @@ constexpr int CW = 16;                                    // epilogue chunk: 16 
 constexpr uint32_t kOutStage = 32 * CW * 4;               // one 32-row x CW fp32 box (64B swizzle)
 constexpr uint32_t kOutStageBytes = 8 * kOutStage;        // <= 8 epilogue warps x 1 transpose box
 // (TMA-store epilogues: nbox boxes per warp, one per output of the chain)
-constexpr int kOtherDepth = 4;                            // max operand boxes in flight per warp
+constexpr int kOtherDepth = 7;                            // max operand boxes in flight per warp
 constexpr uint32_t kOtherBox = 8 * kOutStage;             // one box for each of <= 8 epilogue warps
 constexpr uint32_t kSmemMax = 232448;                     // 227 KB opt-in
-constexpr uint32_t kBarBytes = 1024;
+constexpr uint32_t kBarBytes = 2048;
 constexpr int kSegQ = 8;  // tile queue depth (dynamic schedules)
 
 enum SegKind : int { SEG_WHOLE = 0, SEG_HEAD = 1, SEG_PART = 2 };
@@ -1219,6 +1219,8 @@ bool g_other_loader = true;  // debug (12,0) off / (12,1) on  // debug: per-lane
 int g_split_kb = 0;    // 3xTF32: k-blocks per scheduled segment (debug (13, n); 0 = unbounded)
 int g_split_chain = 2; // 3xTF32: k-blocks per TMEM accumulation chain (debug (14, n); 0 = unbounded)
 bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-in (10,0)
+int g_odepth = 0;      // debug (15, n): operand ring depth n (0 = chosen from the smem budget)
+int g_min_stages = 4;  // debug (16, n): mainloop stages the operand ring must leave
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1318,6 +1320,8 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 3) g_no_3d = (sbo == 1);  // (3,1) MN-major operands as 2-D boxes
   if (lbo == 13) g_split_kb = int(sbo);  // (13,n) 3xTF32 segments of <= n k-blocks (workspace sums)
   if (lbo == 14) g_split_chain = int(sbo) & 15;  // (14,n) 3xTF32 TMEM chains of n k-blocks
+  if (lbo == 15) g_odepth = int(sbo);             // (15,n) epilogue operand ring depth n
+  if (lbo == 16) g_min_stages = int(sbo);         // (16,n) keep >= n mainloop stages
   if (lbo >= 1 && lbo <= 14) g_dbg_lbo = g_dbg_sbo = 0;
 }
 
@@ -1714,9 +1718,10 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   if (g.other_smem) {
     // deepest operand ring that keeps the mainloop's depth (>= 4 stages where possible)
     g.odepth = 1;
-    const int want = std::min(4, stages_for(bn_stage, split, 1, g.nbox));
+    const int want = std::min(g_min_stages, stages_for(bn_stage, split, 1, g.nbox));
     for (int d = kOtherDepth; d > 1; --d)
       if (stages_for(bn_stage, split, d, g.nbox) >= std::max(3, want)) { g.odepth = d; break; }
+    if (g_odepth > 0) g.odepth = std::min(g_odepth, kOtherDepth);
   }
   g.stages = stages_for(bn_stage, split, g.odepth, g.nbox);
   if (g_stages > 0) g.stages = std::min(g.stages, g_stages);

@@ -133,16 +133,80 @@ __device__ __forceinline__ float nary_apply(int op, int nin, const float* v, flo
   }
 }
 
+// ---- peer synchronisation (TPX_FLAG_PEER): system-scope acquire / release on 64-bit counters
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait until every rank in `mask` has reached count `c` (bounded: a wait that outlives
+// timeout_ns records the rank in the host-mapped error word and gives up instead of hanging).
+__device__ void peer_wait(const PeerSync& s, uint32_t mask, unsigned long long c) {
+  for (int r = 0; r < s.world; ++r) {
+    if (!(mask >> r & 1u)) continue;
+    const unsigned long long* p = s.peer[r];
+    if (ld_acquire_sys(p) >= c) continue;
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(p) < c) {
+      if (*reinterpret_cast<volatile int*>(s.err)) return;
+      __nanosleep(200);
+      if (globaltimer() - t0 > s.timeout_ns) {
+        atomicExch(s.err, 0x100 | r);
+        return;
+      }
+    }
+  }
+}
+
+__global__ void sync_kernel(PeerSync s, int barrier) {
+  if (threadIdx.x != 0) return;
+  // everything earlier on this stream (previous launches) is complete: publish it
+  const unsigned long long c = *s.local + 1;
+  __threadfence_system();
+  st_release_sys(s.local, c);
+  if (barrier) peer_wait(s, ((1u << s.world) - 1u) & ~(1u << s.rank), c);
+}
+
+// Chained elementwise stage (EpiOp codes, gemm.h) on the previous stage's stored value.
+__device__ __forceinline__ float chain_apply(int op, float x, float o, float s) {
+  switch (op) {
+    case 1: return tanhf(x);
+    case 2: { const float t = tanhf(x); return 1.0f - t * t; }
+    case 3: return s * x;
+    case 4: return x + o;
+    case 5: return x - o;
+    case 6: return o - x;
+    default: return x;
+  }
+}
 template <class T>
-__global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restrict__ ds, int n) {
+__device__ __forceinline__ float stored(float v) {
+  if constexpr (sizeof(T) == 2) return __bfloat162float(__float2bfloat16_rn(v));
+  else return v;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restrict__ ds, int n, PeerSync sync) {
   const int di = find_desc(&ds[0].d.tile_begin, sizeof(NaryDev), n, blockIdx.x);
   const NaryDev& D = ds[di];
   const NaryDesc& d = D.d;
+  if (d.wait_mask) {  // peer pull: the sources on other ranks must be complete
+    if (threadIdx.x == 0) peer_wait(sync, d.wait_mask, *sync.local);
+    __syncthreads();
+  }
   const int64_t local = int64_t(blockIdx.x) - d.tile_begin;
   const int64_t rb = local / D.n_col_chunks, cc = local % D.n_col_chunks;
   const int64_t r0 = rb * D.rpt, r1 = min(D.rows, r0 + D.rpt);
   const int64_t c0 = cc * D.col_chunk, c1 = min(D.inner, c0 + D.col_chunk);
-  const int nin = d.nin, op = d.op;
+  const int nin = d.nin, op = d.op, nch = d.n_chain;
   // one row per warp; a block holding a single (long) row spreads it over all its threads
   const bool one = (r1 - r0) == 1;
   const int warp = one ? 0 : int(threadIdx.x >> 5), lane = one ? int(threadIdx.x) : int(threadIdx.x & 31);
@@ -152,7 +216,8 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
     const int64_t t = r / d.shape[2];
     const int64_t i1 = t % d.shape[1];
     const int64_t i0 = t / d.shape[1];
-    T* out = reinterpret_cast<T*>(d.out) + i0 * d.out_st[0] + i1 * d.out_st[1] + i2 * d.out_st[2];
+    const int64_t ooff = i0 * d.out_st[0] + i1 * d.out_st[1] + i2 * d.out_st[2];
+    T* out = reinterpret_cast<T*>(d.out) + ooff;
     const T* in[kMaxIn];
 #pragma unroll
     for (int k = 0; k < kMaxIn; ++k)
@@ -183,6 +248,17 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
           o.w = nary_apply(op, nin, a, d.scale);
         }
         est4(out + 4 * c, o);
+        for (int s = 0; s < nch; ++s) {
+          const ChainStage& cs = d.chain[s];
+          const int64_t e = ooff + 4 * c;
+          float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (cs.other) w = eld4(reinterpret_cast<const T*>(cs.other) + e);
+          o.x = chain_apply(cs.op, stored<T>(o.x), w.x, cs.scale);
+          o.y = chain_apply(cs.op, stored<T>(o.y), w.y, cs.scale);
+          o.z = chain_apply(cs.op, stored<T>(o.z), w.z, cs.scale);
+          o.w = chain_apply(cs.op, stored<T>(o.w), w.w, cs.scale);
+          est4(reinterpret_cast<T*>(cs.out) + e, o);
+        }
       }
     } else {
       const int64_t os = d.out_st[3];
@@ -190,8 +266,17 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
         float a[kMaxIn];
 #pragma unroll
         for (int k = 0; k < kMaxIn; ++k) a[k] = k < nin ? eld(in[k] + c * d.in_st[k][3]) : 0.f;
-        if (op == NARY_ACC) est(out + c * os, eldv(out + c * os) + a[0]);
-        else est(out + c * os, nary_apply(op, nin, a, d.scale));
+        float o;
+        if (op == NARY_ACC) o = eldv(out + c * os) + a[0];
+        else o = nary_apply(op, nin, a, d.scale);
+        est(out + c * os, o);
+        for (int s = 0; s < nch; ++s) {
+          const ChainStage& cs = d.chain[s];
+          const int64_t e = ooff + c * os;
+          const float w = cs.other ? eld(reinterpret_cast<const T*>(cs.other) + e) : 0.f;
+          o = chain_apply(cs.op, stored<T>(o), w, cs.scale);
+          est(reinterpret_cast<T*>(cs.out) + e, o);
+        }
       }
     }
   }
@@ -610,7 +695,9 @@ void nary_prepare(NaryBatch& b) {
     tiles += ((rows + t.rpt - 1) / t.rpt) * t.n_col_chunks;
     dev[i] = NaryDev{d, t.rows, t.inner, t.rpt, t.col_chunk, t.n_col_chunks};
     const double elems = double(d.units) * d.vec;
-    b.bytes += (b.bf16 ? 2.0 : 4.0) * elems * (d.nin + 1 + (d.op == NARY_ACC ? 1 : 0));
+    int streams = d.nin + 1 + (d.op == NARY_ACC ? 1 : 0);
+    for (int c = 0; c < d.n_chain; ++c) streams += 1 + (d.chain[c].other ? 1 : 0);
+    b.bytes += (b.bf16 ? 2.0 : 4.0) * elems * streams;
   }
   b.tiles = tiles;
   upload(dev, &b.d_descs);
@@ -620,11 +707,40 @@ void nary_run(const NaryBatch& b, cudaStream_t s) {
   if (!b.tiles) return;
   if (b.bf16)
     nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
-                                                                      int(b.descs.size()));
+                                                                      int(b.descs.size()), b.sync);
   else
     nary_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
-                                                              int(b.descs.size()));
+                                                              int(b.descs.size()), b.sync);
   CUDA_CHECK(cudaGetLastError());
+}
+
+void sync_signal(const PeerSync& s, bool barrier, cudaStream_t st) {
+  sync_kernel<<<1, 32, 0, st>>>(s, barrier ? 1 : 0);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+bool nary_add_chain(NaryDesc& d, const StridedView& d_out, int op, float scale, const StridedView& out,
+                    const StridedView* other, int esize) {
+  if (d.n_chain >= kMaxChain || d.op == NARY_ACC) return false;
+  auto same = [&](const StridedView& v) {
+    if (v.rank != d_out.rank) return false;
+    for (int i = 0; i < v.rank; ++i)
+      if (v.shape[i] != d_out.shape[i] || (v.shape[i] != 1 && v.st[i] != d_out.st[i])) return false;
+    return true;
+  };
+  if (!same(out) || (other && !same(*other))) return false;
+  const uintptr_t al = uintptr_t(4 * esize - 1);
+  if (d.vec == 4 && ((reinterpret_cast<uintptr_t>(out.ptr) & al) ||
+                     (other && (reinterpret_cast<uintptr_t>(other->ptr) & al))))
+    return false;
+  ChainStage& c = d.chain[d.n_chain++];
+  c.op = op;
+  c.scale = scale;
+  // stage views share d_out's layout, so they are indexed with the descriptor's (merged)
+  // output strides relative to their own base
+  c.out = out.ptr;
+  c.other = other ? other->ptr : nullptr;
+  return true;
 }
 
 void nary_free(NaryBatch& b) {

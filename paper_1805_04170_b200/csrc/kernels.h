@@ -15,6 +15,8 @@ namespace tpx {
 
 constexpr int kMaxRank = 4;
 constexpr int kMaxIn = 8;
+constexpr int kMaxChain = 3;
+constexpr int kMaxRanks = 8;
 
 enum NaryOp : int {
   NARY_COPY = 0,   // out = in0
@@ -41,6 +43,18 @@ struct StridedView {
   bool contiguous() const;
 };
 
+// An elementwise stage chained onto an n-ary result (EpiOp codes of gemm.h: tanh, 1 - tanh^2,
+// scale, add, sub): reads the previous stage's STORED value, writes `out`, which has the layout
+// of the descriptor's output (so has `other`).  Used to fuse the consumers of a partial-sum
+// reduction (the SGD step + update of a reduced gradient, the activation of a reduced
+// pre-activation) into the reduction's launch.
+struct ChainStage {
+  int op = 0;
+  float scale = 0.f;
+  float* out = nullptr;
+  const float* other = nullptr;
+};
+
 struct NaryDesc {
   int op = NARY_COPY;
   int nin = 1;
@@ -53,10 +67,30 @@ struct NaryDesc {
   int64_t in_st[kMaxIn][kMaxRank];
   int64_t tile_begin;   // prefix over the batch (filled by nary_prepare)
   int64_t units;        // number of vec-wide units
+  int n_chain;          // chained elementwise stages (0 = none)
+  ChainStage chain[kMaxChain];
+  uint32_t wait_mask;   // peer pull: ranks whose sync counter must reach this rank's first
 };
+
+// Cross-rank ordering of peer-pull steps (TPX_FLAG_PEER).  Every rank owns one 64-bit sync
+// counter at the start of its arena; the other ranks map that arena (CUDA IPC over NVLink).
+// A signal step bumps the local counter after everything earlier on the stream; a pull waits
+// until each rank it reads from has reached the local count (acquire at system scope), so the
+// data it reads is complete.  A barrier (signal + wait for every rank) ends each step, so no
+// rank overwrites a value another rank may still be reading.
+struct PeerSync {
+  unsigned long long* local = nullptr;
+  const unsigned long long* peer[kMaxRanks] = {};
+  int* err = nullptr;                   // host-mapped: 0x100 | rank on a wait that timed out
+  int world = 1, rank = 0;
+  unsigned long long timeout_ns = 0;
+};
+void sync_signal(const PeerSync& s, bool barrier, cudaStream_t st);
 
 struct NaryBatch {
   bool bf16 = false;  // storage type of every operand (arithmetic is fp32)
+  bool pull = false;  // some descriptor reads peer memory (waits on PeerSync first)
+  PeerSync sync;
   std::vector<NaryDesc> descs;
   void* d_descs = nullptr;
   int64_t tiles = 0;
@@ -66,6 +100,11 @@ struct NaryBatch {
 // Build a descriptor: out[i] = op(in_0[i], ...), all views of equal shape.
 NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView>& ins,
                    float scale = 0.f, int esize = 4);
+// Chain an elementwise stage onto d (see ChainStage): `out` (and `other`, for add / sub) must
+// have the shape and strides of `d_out`, the view d was built for.  False when the layouts or
+// the alignment of the 4-wide path do not allow it (the caller then runs the op unfused).
+bool nary_add_chain(NaryDesc& d, const StridedView& d_out, int op, float scale, const StridedView& out,
+                    const StridedView* other, int esize);
 void nary_prepare(NaryBatch& b);  // uploads descriptor table
 void nary_run(const NaryBatch& b, cudaStream_t s);
 void nary_free(NaryBatch& b);

@@ -1,6 +1,7 @@
 #include "runtime.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <sstream>
@@ -98,8 +99,25 @@ struct Lowerer {
   std::map<int, PostTail> post_tail;
   std::vector<int> gemm_step;  // gemm batch -> step index (-1 while open)
 
+  // fetch node -> the reduce_partial that reads its source region in place (no copy of its own)
+  std::vector<int> red_src;
+  struct Direct {
+    StridedView view;  // the piece's region of its source value (on its owner's arena)
+    int src = -1;      // source node (local readiness)
+    int rank = -1;     // owning rank when read from a peer (waits on its sync counter), else -1
+  };
+  std::map<int, Direct> direct;
+  // reduce_partial (or a fused consumer of one) -> the descriptor its elementwise consumers chain
+  // onto: (nary batch, descriptor, step, the reduction's output view)
+  struct RedTail {
+    int batch, desc, step;
+    StridedView out;
+  };
+  std::map<int, RedTail> red_tail;
+  std::vector<int> open_red;   // reductions in the open reduce batch (tail candidates)
+
   // open segment
-  NaryBatch o_pre, o_ew, o_pack, o_copy, o_reduce;
+  NaryBatch o_pre, o_ew, o_pack, o_copy, o_reduce, o_pull;
   ConvBatch o_prec, o_post;    // im2col before / col2im after a conv's GEMM
   XchgGroup o_xchg;
   int o_gemm = -1;             // open gemm batch index
@@ -156,6 +174,24 @@ struct Lowerer {
            (reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0;
   }
 
+  // Value of `node` on rank `r` as this rank addresses it: its own value, or (peer mode) the view
+  // a host-only lowering of the plan as rank r gave it, moved onto r's mapped arena.
+  StridedView src_view(int r, int node) {
+    if (r == C.rank) return value(node);
+    const PlanNode& n = pl.nodes[size_t(node)];
+    if (dry) return contiguous_view(reinterpret_cast<float*>(kFakeBase), n.region.shape());
+    if (size_t(r) >= P.rhas.size() || !P.rhas[size_t(r)][size_t(node)])
+      fail("node " + n.id + " has no value on rank " + std::to_string(r));
+    StridedView v = (swap_to ? P.rval_b : P.rval)[size_t(r)][size_t(node)];
+    v.ptr = reinterpret_cast<float*>(P.peer_base[size_t(r)] + (reinterpret_cast<uintptr_t>(v.ptr) - kFakeBase));
+    return v;
+  }
+  void sync_step(bool barrier) {
+    flush();
+    const int s = add_step(ST_SYNC, 0, barrier ? std::string() : seg_op, barrier ? "barrier" : "signal");
+    prog.steps[size_t(s)].barrier = barrier ? 1 : 0;
+  }
+
   int rank_of(int dev) const { return P.dev_rank[size_t(dev)]; }
   bool mine_dev(int dev) const { return rank_of(dev) == C.rank; }
 
@@ -206,6 +242,8 @@ struct Lowerer {
     }
     post_open.clear();
     emit_nary(o_pack, seg_op, "pack", C_PACK);
+    if (!o_pull.descs.empty()) o_pull.pull = true;
+    emit_nary(o_pull, seg_op, "pull", C_XCHG);
     if (!o_xchg.x.empty()) {
       prog.xchg.push_back(std::move(o_xchg));
       o_xchg = XchgGroup{};
@@ -213,7 +251,16 @@ struct Lowerer {
       for (int n : o_nodes[C_XCHG]) P.avail_step[size_t(n)] = s;
     }
     emit_nary(o_copy, seg_op, "copy", C_COPY);
+    const bool had_reduce = !o_reduce.descs.empty();
     emit_nary(o_reduce, seg_op, "reduce", C_REDUCE);
+    if (had_reduce) {
+      for (int r : open_red) {
+        RedTail& t = red_tail[r];
+        t.batch = int(prog.nary.size()) - 1;
+        t.step = int(prog.steps.size()) - 1;
+      }
+    }
+    open_red.clear();
     for (int c = 0; c < C_N; ++c) {
       for (int n : o_nodes[c]) pending[size_t(n)] = -1;
       o_nodes[c].clear();
@@ -263,7 +310,7 @@ struct Lowerer {
     if (op.kind == OpKind::generic)
       fail("op '" + op.id + "': unbound function tag (generic ops have no numeric binding)");
 
-    if (op.kind == OpKind::elementwise && fuse && try_fuse(ni, op)) return;
+    if (op.kind == OpKind::elementwise && fuse && (try_fuse_reduce(ni, op) || try_fuse(ni, op))) return;
 
     if (op.kind == OpKind::conv && tc_conv) {
       lower_conv_gemm(ni, op);
@@ -652,6 +699,49 @@ struct Lowerer {
       P.op_bytes_in[op_of_phase(n.phase)] += n.bytes;
       P.phase_bytes_in[n.phase] += n.bytes;
     }
+    const int sr = rank_of(sn.device);
+    if (red_src[size_t(ni)] >= 0 && (!remote || P.peer())) {
+      // read in place by the reduction that consumes it (no copy, no staging)
+      const size_t bytes = size_t(n.region.volume()) * size_t(g_es);
+      if (src_mine && rank_of(n.device) != C.rank) P.xrank_out += int64_t(bytes);
+      if (!dst_mine) return;
+      if (sr != C.rank) {
+        P.xrank_in += int64_t(bytes);
+        P.pull_bytes += int64_t(bytes);
+      }
+      Direct d;
+      d.view = subview(src_view(sr, src), sn.region, n.region);
+      d.src = src;
+      d.rank = remote ? sr : -1;
+      direct[ni] = d;
+      return;
+    }
+    if (remote && P.peer()) {
+      // peer pull: this rank reads the piece out of the owner's arena (pack + NVLink transfer +
+      // unpack in one pass); the owner does nothing
+      const size_t bytes = size_t(n.region.volume()) * size_t(g_es);
+      if (src_mine && rank_of(n.device) != C.rank) P.xrank_out += int64_t(bytes);
+      if (!dst_mine) return;
+      if (sr != C.rank) {
+        P.xrank_in += int64_t(bytes);
+        P.pull_bytes += int64_t(bytes);
+      } else {
+        need(src, C_XCHG);
+      }
+      const StridedView sv = subview(src_view(sr, src), sn.region, n.region);
+      StridedView target;
+      if (cat >= 0) {
+        ensure_alloc(cat);
+        target = subview(P.val[size_t(cat)], pl.nodes[size_t(cat)].region, n.region);
+      } else {
+        target = set_val(ni, alloc(n.region.shape()));
+        produced(ni, C_XCHG);
+      }
+      NaryDesc d = ndesc(NARY_COPY, target, {sv});
+      d.wait_mask = 1u << sr;
+      o_pull.descs.push_back(d);
+      return;
+    }
     if (!remote) {
       if (!dst_mine) return;
       if (n.kind == NodeKind::slice && cat < 0) {
@@ -730,7 +820,15 @@ struct Lowerer {
     const PlanNode& n = pl.nodes[size_t(ni)];
     if (!mine_dev(n.device)) return;
     std::vector<StridedView> ins;
+    uint32_t mask = 0;
     for (int s : n.sources) {
+      auto it = direct.find(s);
+      if (it != direct.end()) {  // a fetched partial read where it lies (local or on its peer)
+        if (it->second.rank >= 0) mask |= 1u << it->second.rank;
+        else need(it->second.src, C_REDUCE);
+        ins.push_back(it->second.view);
+        continue;
+      }
       need(s, C_REDUCE);
       ins.push_back(value(s));
     }
@@ -738,18 +836,79 @@ struct Lowerer {
     // Sum in source order (execgraph.cpp:264-282 fixes that order).  More than 8 partials
     // (k > 3) continue as out = out + next 7 in a following launch.
     size_t i = std::min(ins.size(), size_t(kMaxIn));
-    o_reduce.descs.push_back(ndesc(i == 1 ? NARY_COPY : NARY_SUM, out,
-                                       std::vector<StridedView>(ins.begin(), ins.begin() + long(i))));
+    NaryDesc d0 = ndesc(i == 1 ? NARY_COPY : NARY_SUM, out, std::vector<StridedView>(ins.begin(), ins.begin() + long(i)));
+    d0.wait_mask = mask;
+    if (mask) o_reduce.pull = true;
+    o_reduce.descs.push_back(d0);
+    if (i == ins.size() && fuse) {
+      red_tail[ni] = RedTail{-1, int(o_reduce.descs.size()) - 1, -1, out};
+      open_red.push_back(ni);
+    }
     while (i < ins.size()) {
       produced(ni, C_REDUCE);
       flush();
       const size_t j = std::min(ins.size(), i + kMaxIn - 1);
       std::vector<StridedView> chunk{out};
       chunk.insert(chunk.end(), ins.begin() + long(i), ins.begin() + long(j));
-      o_reduce.descs.push_back(ndesc(NARY_SUM, out, chunk));
+      NaryDesc d = ndesc(NARY_SUM, out, chunk);
+      d.wait_mask = mask;
+      if (mask) o_reduce.pull = true;
+      o_reduce.descs.push_back(d);
       i = j;
     }
     produced(ni, C_REDUCE);
+  }
+
+  // Elementwise consumer of a (finished) reduction, chained onto the reduction's launch: it reads
+  // the sum's stored value in registers instead of from HBM (K4: partial-sum reduce fused with
+  // the SGD step + update, or with the activation of a reduced pre-activation).
+  bool try_fuse_reduce(int ni, const OpSpec& op) {
+    const PlanNode& n = pl.nodes[size_t(ni)];
+    int j_tail = -1;
+    for (size_t j = 0; j < n.sources.size(); ++j) {
+      auto it = red_tail.find(n.sources[j]);
+      if (it != red_tail.end() && it->second.batch >= 0) {
+        j_tail = int(j);
+        break;
+      }
+    }
+    if (j_tail < 0) return false;
+    const int src = n.sources[size_t(j_tail)];
+    const RedTail t = red_tail[src];
+    int code = 0;
+    switch (op.fn) {
+      case EwFn::pointwise_fn: code = EPI_TANH; break;
+      case EwFn::pointwise_fn_grad: code = EPI_DTANH; break;
+      case EwFn::scale: code = EPI_SCALE; break;
+      case EwFn::add: code = EPI_ADD; break;
+      case EwFn::sub: code = j_tail == 0 ? EPI_SUB_PO : EPI_SUB_OP; break;
+    }
+    const StridedView* other = nullptr;
+    StridedView ov;
+    if (n.sources.size() == 2) {
+      const int o = n.sources[size_t(1 - j_tail)];
+      if (o == src || pending[size_t(o)] >= 0 || P.avail_step[size_t(o)] >= t.step) return false;
+      ov = value(o);
+      other = &ov;
+    } else if (n.sources.size() != 1) {
+      return false;
+    }
+    if (n.region.shape() != pl.nodes[size_t(src)].region.shape()) return false;
+    NaryDesc& d = prog.nary[size_t(t.batch)].descs[size_t(t.desc)];
+    // (loop mode: a weight's w_next may take the weight's storage -- same layout -- and the
+    // fresh allocation stays unused, so both programs allocate alike)
+    StridedView out = alloc(n.region.shape());
+    if (swap_to) {
+      auto it = swap_to->find(ni);
+      if (it != swap_to->end()) out = it->second;
+    }
+    if (!nary_add_chain(d, t.out, code, float(op.scale), out, other, g_es)) return false;
+    set_val(ni, out);
+    red_tail.erase(src);
+    red_tail[ni] = t;
+    P.avail_step[size_t(ni)] = t.step;
+    P.n_fused++;
+    return true;
   }
 
   void lower_buffer(int ni) {
@@ -795,6 +954,7 @@ struct Lowerer {
         consumers[size_t(s)]++;
         last_consumer[size_t(s)] = int(i);
       }
+    red_src.assign(N, -1);
     for (size_t i = 0; i < N; ++i) {
       const PlanNode& n = pl.nodes[i];
       if ((n.kind == NodeKind::fetch || n.kind == NodeKind::slice) && consumers[i] == 1 &&
@@ -802,10 +962,21 @@ struct Lowerer {
         const int c = last_consumer[i];
         if (pl.nodes[size_t(c)].kind == NodeKind::concat && pl.nodes[size_t(c)].device == n.device)
           defer_to[i] = c;
+        if (n.kind == NodeKind::fetch && fuse && pl.nodes[size_t(c)].kind == NodeKind::reduce_partial &&
+            pl.nodes[size_t(c)].device == n.device)
+          red_src[i] = c;
       }
     }
+    // peer mode: every rank signals at the first conversion node of each phase in which any rank
+    // pulls from another (the same sequence of sync points on every rank)
+    std::set<std::string> xph;
+    if (P.peer())
+      for (const auto& n : pl.nodes)
+        if (n.kind == NodeKind::fetch &&
+            (rank_of(n.device) != rank_of(pl.nodes[size_t(n.sources[0])].device) || force_xchg))
+          xph.insert(n.phase);
     std::string cur_phase;
-    bool seen_conv = false;
+    bool seen_conv = false, synced = false;
     for (size_t i = 0; i < N; ++i) {
       const PlanNode& n = pl.nodes[i];
       if (n.phase != cur_phase) {
@@ -813,6 +984,11 @@ struct Lowerer {
         cur_phase = n.phase;
         seg_op = op_of_phase(n.phase);
         seen_conv = false;
+        synced = false;
+      }
+      if (!synced && n.kind != NodeKind::sub_op && n.kind != NodeKind::buffer && xph.count(n.phase)) {
+        sync_step(false);  // after this phase's compute, before any of its pulls
+        synced = true;
       }
       switch (n.kind) {
         case NodeKind::buffer: lower_buffer(int(i)); break;
@@ -827,11 +1003,15 @@ struct Lowerer {
       }
     }
     flush();
+    if (!xph.empty()) {
+      sync_step(true);  // no rank starts the next step while another may still read this one
+    }
   }
 
   // Loop carry: every "<w>_next" holder block onto the holder blocks of weight "<w>" (weights
   // carried by the loop-mode swap excepted).
   void run_carry() {
+    bool any_pull = false;
     for (const auto& kv : pl.tensors) {
       const std::string& id = kv.first;
       if (id.size() <= 5 || id.compare(id.size() - 5, 5, "_next") != 0) continue;
@@ -892,6 +1072,19 @@ struct Lowerer {
           const size_t bytes = size_t(pc.first.volume()) * size_t(g_es);
           const bool remote = rank_of(e) != rank_of(d) || (force_xchg && e != d);
           if (e != d) P.carry_bytes += int64_t(bytes);
+          if (remote && P.peer()) {
+            // pulled by the destination out of the owner's arena; the main program's closing
+            // barrier already ordered every rank's w_next before this read
+            any_pull = true;
+            if (mine_dev(e) && rank_of(d) != C.rank) P.carry_xrank += int64_t(bytes);
+            if (!mine_dev(d)) continue;
+            const int sr = rank_of(e);
+            NaryDesc nd = ndesc(NARY_COPY, subview(P.val[size_t(dn)], dnode.region, pc.first),
+                                {subview(src_view(sr, sn), snode.region, pc.first)});
+            nd.wait_mask = 1u << sr;
+            o_pull.descs.push_back(nd);
+            continue;
+          }
           if (!remote) {
             if (!mine_dev(d)) continue;
             copy_into(subview(P.val[size_t(dn)], dnode.region, pc.first),
@@ -924,6 +1117,7 @@ struct Lowerer {
     }
     seg_op = "carry";
     flush();
+    if (any_pull) sync_step(true);  // the next step overwrites w_next only after every pull
   }
 };
 
@@ -974,8 +1168,8 @@ void lower(PlanRt& P, bool dry) {
   P.val.assign(P.plan.nodes.size(), StridedView{});
   P.has_val.assign(P.plan.nodes.size(), 0);
   P.avail_step.assign(P.plan.nodes.size(), -1);
-  P.arena_used = 0;
-  P.fetch_in = P.xrank_in = P.xrank_out = P.carry_bytes = P.carry_xrank = 0;
+  P.arena_used = P.peer() ? kAlign : 0;  // peer mode: the sync counter lives at the arena base
+  P.fetch_in = P.xrank_in = P.xrank_out = P.carry_bytes = P.carry_xrank = P.pull_bytes = 0;
   P.n_fused = 0;
   P.op_bytes_in.clear();
   P.phase_bytes_in.clear();
@@ -1000,11 +1194,11 @@ void lower(PlanRt& P, bool dry) {
     sv_avail.swap(P.avail_step);
     const size_t used = P.arena_used;
     const auto acct = std::make_tuple(P.fetch_in, P.xrank_in, P.xrank_out, P.n_fused, P.op_bytes_in, P.phase_bytes_in,
-                                      P.gemm_flops, P.gemm_min_bytes);
+                                      P.gemm_flops, P.gemm_min_bytes, P.pull_bytes);
     P.val.assign(P.plan.nodes.size(), StridedView{});
     P.has_val.assign(P.plan.nodes.size(), 0);
     P.avail_step.assign(P.plan.nodes.size(), -1);
-    P.arena_used = 0;
+    P.arena_used = P.peer() ? kAlign : 0;
     InitBatch init_a = std::move(P.init);
     P.init = InitBatch{};
     {
@@ -1019,19 +1213,22 @@ void lower(PlanRt& P, bool dry) {
     P.has_val.swap(sv_has);
     P.avail_step.swap(sv_avail);
     std::tie(P.fetch_in, P.xrank_in, P.xrank_out, P.n_fused, P.op_bytes_in, P.phase_bytes_in, P.gemm_flops,
-             P.gemm_min_bytes) = acct;
+             P.gemm_min_bytes, P.pull_bytes) = acct;
   }
   {
     Lowerer L(P, P.carry, dry);
     L.pending.assign(P.plan.nodes.size(), -1);
     L.run_carry();
   }
+  P.n_sync = 0;
+  for (const auto& st : P.main.steps) P.n_sync += st.kind == ST_SYNC;
 }
 
 void prepare_program(PlanRt& P, Program& prog) {
   const bool bf = P.esize == 2;
   for (auto& b : prog.nary) {
     b.bf16 = bf;
+    if (b.pull) b.sync = P.sync;
     nary_prepare(b);
   }
   for (auto& b : prog.conv) {
@@ -1063,6 +1260,8 @@ PlanRt::~PlanRt() {
   init_free(init);
   for (auto e : events) cudaEventDestroy(e);
   if (io_tmp) cudaFree(io_tmp);
+  for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+  if (err_host) cudaFreeHost(err_host);
   if (arena) cudaFree(arena);
 }
 
@@ -1095,9 +1294,11 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
   for (int d = 0; d < devices; ++d) P->dev_rank[size_t(d)] = int((int64_t(d) * ctx->world) / devices);
   lower(*P, true);
   if (!ctx->host_only()) {
-    if ((flags & 2) || ctx->world > 1) {
+    if (P->peer()) {
+      if (ctx->world > kMaxRanks) fail("peer mode supports at most " + std::to_string(kMaxRanks) + " ranks");
+    } else if ((flags & 2) || ctx->world > 1) {
       if (!ctx->comm) {
-        if (ctx->world > 1) fail("multi-rank plan needs tpx_init_comm first");
+        if (ctx->world > 1) fail("multi-rank plan needs tpx_init_comm first (or TPX_FLAG_PEER)");
         char uid[128];
         nccl_unique_id(uid);
         ctx->comm = nccl_comm_init(1, uid, 0);
@@ -1106,19 +1307,101 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
     P->arena_bytes = std::max<size_t>(P->arena_used, kAlign);
     CUDA_CHECK(cudaMalloc(&P->arena, P->arena_bytes));
     // scratch padding (16-byte rows of im2col matrices, per-image column blocks) is read as
-    // zero by the GEMMs and never written
+    // zero by the GEMMs and never written; the peer-mode sync counter starts at 0
     CUDA_CHECK(cudaMemset(P->arena, 0, P->arena_bytes));
     P->base = reinterpret_cast<uintptr_t>(P->arena);
+    if (P->peer()) {
+      CUDA_CHECK(cudaHostAlloc(&P->err_host, sizeof(int), cudaHostAllocMapped));
+      *P->err_host = 0;
+      int* err_dev = nullptr;
+      CUDA_CHECK(cudaHostGetDevicePointer(&err_dev, P->err_host, 0));
+      P->sync.local = reinterpret_cast<unsigned long long*>(P->arena);
+      P->sync.err = err_dev;
+      P->sync.world = ctx->world;
+      P->sync.rank = ctx->rank;
+      const char* to = std::getenv("TPX_PEER_TIMEOUT_S");
+      P->sync.timeout_ns = static_cast<unsigned long long>((to ? std::atof(to) : 60.0) * 1e9);
+      P->sync.peer[ctx->rank] = P->sync.local;
+      P->peer_base.assign(size_t(ctx->world), 0);
+      P->peer_base[size_t(ctx->rank)] = P->base;
+      if (ctx->world > 1) return P.release();  // lowered by connect_peers once the arenas are mapped
+    }
     lower(*P, false);
     prepare_program(*P, P->main);
     prepare_program(*P, P->carry);
     prepare_program(*P, P->main_b);
     P->init.bf16 = P->esize == 2;
     init_prepare(P->init);
+    P->lowered = true;
   } else {
     P->arena_bytes = P->arena_used;
   }
   return P.release();
+}
+
+void arena_ipc_handle(PlanRt& P, void* out, size_t len) {
+  if (!P.peer()) fail("IPC handles are for TPX_FLAG_PEER plans");
+  if (P.ctx->host_only()) fail("host-only context has no arena");
+  if (len < sizeof(cudaIpcMemHandle_t)) fail("IPC handle buffer must hold " + std::to_string(sizeof(cudaIpcMemHandle_t)) + " bytes");
+  cudaIpcMemHandle_t h;
+  CUDA_CHECK(cudaIpcGetMemHandle(&h, P.arena));
+  std::memcpy(out, &h, sizeof h);
+}
+
+void connect_peers(PlanRt& P, const void* handles, size_t len) {
+  if (!P.peer()) fail("connect_peers needs a TPX_FLAG_PEER plan");
+  if (P.lowered) fail("plan is already connected");
+  const int world = P.ctx->world, me = P.ctx->rank;
+  if (len < size_t(world) * sizeof(cudaIpcMemHandle_t))
+    fail("connect_peers needs " + std::to_string(world) + " arena handles (" +
+         std::to_string(size_t(world) * sizeof(cudaIpcMemHandle_t)) + " bytes)");
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int r = 0; r < world; ++r) {
+    if (r == me) continue;
+    void* ptr = nullptr;
+    CUDA_CHECK(cudaIpcOpenMemHandle(&ptr, hs[r], cudaIpcMemLazyEnablePeerAccess));
+    P.ipc_opened.push_back(ptr);
+    P.peer_base[size_t(r)] = reinterpret_cast<uintptr_t>(ptr);
+    P.sync.peer[r] = static_cast<const unsigned long long*>(ptr);
+  }
+  // every other rank's node values, from a host-only lowering of the plan as that rank
+  P.rval.assign(size_t(world), {});
+  P.rval_b.assign(size_t(world), {});
+  P.rhas.assign(size_t(world), {});
+  for (int r = 0; r < world; ++r) {
+    if (r == me) continue;
+    Ctx c2 = *P.ctx;
+    c2.rank = r;
+    c2.ordinal = -1;
+    PlanRt q;
+    q.ctx = &c2;
+    q.plan = P.plan;
+    q.precision = P.precision;
+    q.flags = P.flags;
+    q.esize = P.esize;
+    q.dev_rank = P.dev_rank;
+    lower(q, true);
+    P.rval[size_t(r)].swap(q.val);
+    P.rval_b[size_t(r)].swap(q.val_b);
+    P.rhas[size_t(r)].swap(q.has_val);
+  }
+  const size_t used = P.arena_used;
+  lower(P, false);
+  if (P.arena_used != used) fail("peer lowering is not deterministic");
+  prepare_program(P, P.main);
+  prepare_program(P, P.carry);
+  prepare_program(P, P.main_b);
+  P.init.bf16 = P.esize == 2;
+  init_prepare(P.init);
+  P.lowered = true;
+}
+
+void check_peer_error(PlanRt& P) {
+  if (P.err_host && *P.err_host) {
+    const int e = *P.err_host;
+    fail("peer pull timed out waiting for rank " + std::to_string(e & 0xff) +
+         " (a rank stopped executing the plan, or TPX_PEER_TIMEOUT_S is too short)");
+  }
 }
 
 static void launch_step(PlanRt& P, Program& prog, const Step& s, cudaStream_t st) {
@@ -1126,6 +1409,7 @@ static void launch_step(PlanRt& P, Program& prog, const Step& s, cudaStream_t st
     case ST_NARY: nary_run(prog.nary[size_t(s.idx)], st); break;
     case ST_GEMM: gemm_run(prog.gemm[size_t(s.idx)], st); break;
     case ST_CONV: conv_run(prog.conv[size_t(s.idx)], st); break;
+    case ST_SYNC: sync_signal(P.sync, s.barrier != 0, st); break;
     case ST_XCHG: {
       const XchgGroup& g = prog.xchg[size_t(s.idx)];
       nccl_group_start();
@@ -1141,6 +1425,7 @@ static void launch_step(PlanRt& P, Program& prog, const Step& s, cudaStream_t st
 
 void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
   if (P.ctx->host_only()) fail("host-only context cannot execute plans");
+  if (!P.lowered) fail("peer-mode plan: tpx_plan_connect_peers must run on every rank first");
   cudaStream_t st = P.stream;
   const bool is_main = &prog == &P.main || &prog == &P.main_b;
   if ((P.flags & 8) && !P.timing && !only_op && is_main) {
@@ -1169,8 +1454,8 @@ void run_program(PlanRt& P, Program& prog, const std::string* only_op) {
     return;
   }
   if (!P.timing || only_op || !is_main) {  // per-step timing covers the step's main program
-    for (const auto& s : prog.steps)
-      if (!only_op || s.op == *only_op) launch_step(P, prog, s, st);
+    for (const auto& s : prog.steps)  // (a barrier runs with every op: it ends each call)
+      if (!only_op || s.op == *only_op || (s.kind == ST_SYNC && s.barrier)) launch_step(P, prog, s, st);
     return;
   }
   const size_t n = prog.steps.size();
@@ -1214,6 +1499,7 @@ void run_step(PlanRt& P) {
 
 void run_steps(PlanRt& P, int64_t begin, int64_t end) {
   if (P.ctx->host_only()) fail("host-only context cannot execute plans");
+  if (!P.lowered) fail("peer-mode plan: tpx_plan_connect_peers must run on every rank first");
   // loop mode: the range runs on the program of the current step; the step ends (and the next
   // one uses the other program, after the carry) with the range that reaches the last step
   const int par = P.loop() ? P.parity : 0;
@@ -1277,6 +1563,7 @@ void copy_node_device(PlanRt& P, int node, void* dev, int64_t n, bool to_node) {
 
 void init_inputs(PlanRt& P, uint64_t seed) {
   if (P.ctx->host_only()) fail("host-only context cannot execute plans");
+  if (!P.lowered) fail("peer-mode plan: tpx_plan_connect_peers must run on every rank first");
   P.parity = P.last = 0;  // the inputs are seeded where the first program reads them
   if (P.init.descs.empty()) return;
   // re-key the descriptors with the seed (state0 = seed ^ fnv1a(id), dense.cpp:51)
@@ -1297,6 +1584,7 @@ static void ensure_io(PlanRt& P, int64_t n) {
 
 static const StridedView& node_val(PlanRt& P, int node, int64_t n) {
   if (P.ctx->host_only()) fail("host-only context holds no values");
+  if (!P.lowered) fail("peer-mode plan: tpx_plan_connect_peers must run on every rank first");
   if (!P.has_val[size_t(node)])
     fail("node " + P.plan.nodes[size_t(node)].id + " has no value on this rank");
   const StridedView& v = (P.loop() && P.last == 1) ? P.val_b[size_t(node)] : P.val[size_t(node)];
@@ -1391,14 +1679,23 @@ std::string describe(const PlanRt& P) {
     for (size_t i = 0; i < prog.steps.size(); ++i) {
       const Step& st = prog.steps[i];
       if (i) s << ",";
-      s << "{\"kind\":" << json_quote(st.kind == ST_NARY ? "nary" : st.kind == ST_GEMM ? "gemm" : st.kind == ST_CONV ? "conv" : "nccl")
+      s << "{\"kind\":" << json_quote(st.kind == ST_NARY ? "nary" : st.kind == ST_GEMM ? "gemm" : st.kind == ST_CONV ? "conv" : st.kind == ST_SYNC ? "sync" : "nccl")
         << ",\"op\":" << json_quote(st.op) << ",\"what\":" << json_quote(st.what);
       if (st.kind == ST_NARY) {
         const NaryBatch& b = prog.nary[size_t(st.idx)];
         s << ",\"descs\":" << b.descs.size();
         double bytes = 0;
-        for (const auto& d : b.descs) bytes += double(P.esize) * double(d.units) * d.vec * (d.nin + 1);
-        s << ",\"bytes\":" << int64_t(bytes);
+        int chained = 0;
+        uint32_t mask = 0;
+        for (const auto& d : b.descs) {
+          int streams = d.nin + 1;
+          for (int c = 0; c < d.n_chain; ++c) streams += 1 + (d.chain[c].other ? 1 : 0);
+          bytes += double(P.esize) * double(d.units) * d.vec * streams;
+          chained += d.n_chain;
+          mask |= d.wait_mask;
+        }
+        s << ",\"bytes\":" << int64_t(bytes) << ",\"chained\":" << chained << ",\"pull\":" << (b.pull ? 1 : 0)
+          << ",\"wait_mask\":" << mask;
       } else if (st.kind == ST_GEMM) {
         const auto& specs = prog.gemm_specs[size_t(st.idx)];
         s << ",\"problems\":" << specs.size() << ",\"shapes\":[";
@@ -1435,6 +1732,8 @@ std::string describe(const PlanRt& P) {
         s << "],\"bytes_in\":" << g.bytes_in << ",\"bytes_out\":" << g.bytes_out;
       } else if (st.kind == ST_CONV) {
         s << ",\"descs\":" << prog.conv[size_t(st.idx)].descs.size();
+      } else if (st.kind == ST_SYNC) {
+        s << ",\"barrier\":" << st.barrier;
       }
       s << "}";
     }
@@ -1448,7 +1747,8 @@ std::string describe(const PlanRt& P) {
     << ",\"rank_xrank_bytes_in\":" << P.xrank_in << ",\"rank_xrank_bytes_out\":" << P.xrank_out
     << ",\"carry_bytes\":" << P.carry_bytes << ",\"carry_xrank_bytes_out\":" << P.carry_xrank
     << ",\"fused_elementwise\":" << P.n_fused << ",\"arena_bytes\":" << P.arena_used
-    << ",\"gemm_flops\":" << P.gemm_flops;
+    << ",\"gemm_flops\":" << P.gemm_flops << ",\"peer\":" << (P.peer() ? 1 : 0)
+    << ",\"pull_bytes_in\":" << P.pull_bytes << ",\"sync_points\":" << P.n_sync;
   auto map_json = [&](const std::map<std::string, int64_t>& m) {
     std::ostringstream s;
     s << "{";

@@ -9,9 +9,16 @@
 //   slice                           -> zero-copy strided view (or a copy straight into the
 //                                     concat that consumes it)
 //   fetch (same rank)               -> HBM copy (into the consuming concat when there is one)
-//   fetch (other rank)              -> pack (if strided) + NCCL send/recv group + unpack
+//   fetch (other rank)              -> peer mode (TPX_FLAG_PEER): one pull launch per phase that
+//                                     reads the remote strided boxes straight out of the peer's
+//                                     arena over NVLink (CUDA IPC) and writes them at their place
+//                                     in the consumer: pack + transfer + unpack in one pass;
+//                                     otherwise pack (if strided) + NCCL send/recv group + unpack
 //   concat                          -> one buffer; every piece lands at its offset
-//   reduce_partial                  -> ordered sum of the partials (deterministic)
+//   reduce_partial                  -> ordered sum of the partials (deterministic), reading
+//                                     single-piece partials in place (local or on the peer) and
+//                                     running the elementwise consumers of the sum (SGD step +
+//                                     update, tanh, 1 - tanh^2) in the same launch
 // Every node value is an immutable strided fp32 view into one HBM arena.
 #pragma once
 #include <cstdint>
@@ -36,13 +43,14 @@ struct Ctx {
   bool host_only() const { return ordinal < 0; }
 };
 
-enum StepKind { ST_NARY, ST_GEMM, ST_CONV, ST_XCHG };
+enum StepKind { ST_NARY, ST_GEMM, ST_CONV, ST_XCHG, ST_SYNC };
 
 struct Step {
   StepKind kind;
   int idx;             // into the batch vector of that kind
   std::string op;      // owning op id (phase prefix)
   std::string what;    // "pack" / "copy" / "reduce" / "ew" / "materialize" / "gemm" ...
+  int barrier = 0;     // ST_SYNC: 1 = end-of-step barrier (signal + wait for every rank)
 };
 
 struct Xfer {
@@ -94,6 +102,20 @@ struct PlanRt {
   int last = 0;                          // program whose values the node reads see
   bool loop() const { return (flags & 16) != 0; }
   InitBatch init;
+  // TPX_FLAG_PEER: cross-rank fetches are pulled from the peers' arenas (CUDA IPC mappings);
+  // peer_base[r] = rank r's arena as mapped in this process (own arena for r == rank).  The
+  // other ranks' node values come from a host-only lowering of the plan as that rank
+  // (deterministic), stored relative to the dry-run base.
+  bool peer() const { return (flags & 32) != 0; }
+  std::vector<uintptr_t> peer_base;
+  std::vector<std::vector<StridedView>> rval, rval_b;
+  std::vector<std::vector<char>> rhas;
+  std::vector<void*> ipc_opened;
+  bool lowered = false;            // real (non-dry) lowering done
+  int n_sync = 0;                  // sync points per step (signals + barrier)
+  PeerSync sync;
+  int* err_host = nullptr;         // host-mapped error word of the peer waits
+  int64_t pull_bytes = 0;          // bytes this rank pulls from other ranks per step
   // accounting
   int64_t fetch_in = 0, xrank_in = 0, xrank_out = 0, carry_bytes = 0, carry_xrank = 0;
   int n_fused = 0;
@@ -117,6 +139,12 @@ struct PlanRt {
 };
 
 PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags);
+// Peer mode with several ranks: the CUDA IPC handle of this rank's arena, and the second half of
+// the load once every rank's handle is known (maps the peers' arenas, lowers, prepares).
+void arena_ipc_handle(PlanRt& p, void* out, size_t len);
+void connect_peers(PlanRt& p, const void* handles, size_t len);
+// Throws if a peer wait timed out (call after a stream synchronisation).
+void check_peer_error(PlanRt& p);
 void run_program(PlanRt& p, Program& prog, const std::string* only_op);
 // One train step: main (or, in loop mode, main / main_b alternately), then the carry program
 // when the plan has weights the swap cannot carry (loop mode only).

@@ -31,6 +31,7 @@ FLAG_FORCE_XCHG = 2
 FLAG_DIRECT_CONV = 4  # convolutions as direct CUDA-core loops (cross-check of the tcgen05 lowering)
 FLAG_GRAPH = 8        # the whole step replayed as one CUDA graph
 FLAG_LOOP = 16        # execute() = one training-loop step: the weights carry into the next step
+FLAG_PEER = 32        # cross-rank fetches pulled from the peers' arenas over NVLink (CUDA IPC)
 
 
 @dataclass
@@ -95,6 +96,24 @@ class PlanExecutor:
         self._h = h
         self.plan = json.loads(self.plan_text)
         self._nodes = {n["id"]: n for n in self.plan["nodes"]}
+
+    # ---------------------------------------------------------------- peer mode
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        check(lib().tpx_plan_ipc_handle(self._h, buf, 64))
+        return buf.raw
+
+    def connect_peers(self, handles: List[bytes]):
+        raw = b"".join(handles)
+        check(lib().tpx_plan_connect_peers(self._h, raw, len(raw)))
+
+    def connect_peers_from_torch(self, group=None):
+        """FLAG_PEER with world > 1: all-gather the arenas' 64-byte CUDA IPC handles over the
+        torch.distributed group (plumbing only) and map the peers' arenas."""
+        import torch.distributed as dist
+        handles = [None] * self.ctx.world
+        dist.all_gather_object(handles, self.ipc_handle(), group=group)
+        self.connect_peers(handles)
 
     # ---------------------------------------------------------------- lifecycle
     def close(self):

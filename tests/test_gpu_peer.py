@@ -1,0 +1,230 @@
+"""GPU checks of the peer-pull exchange (TPX_FLAG_PEER) and of the fused reduce + SGD.
+
+1. One rank, every cross-device fetch forced through the peer path (FORCE_XCHG | PEER: pulls
+   against the rank's own arena, device-side sync counters, closing barrier): every holder
+   is bit-identical to the HBM-copy lowering of the same plan, eagerly and as a replayed CUDA
+   graph, in TF32, fp32-accurate and bf16 plans.
+2. Two ranks on ONE GPU (two processes, each its own CUDA context; the arenas shared by CUDA IPC
+   exactly as across NVLink; gloo only carries the 64-byte handles): the real multi-rank data
+   path — pulls out of the other process's arena, cross-process counters, barrier per step.
+   Every holder matches the oracle (the numpy restatement of execute_numeric pinned to the
+   reference's golden vectors) within the chained fp32 gate, and every fetched piece equals its source region on the other rank
+   bit for bit.  Loop mode (weights carried across steps by buffer swap / carry program) runs
+   three steps and must equal three single steps run with an explicit carry.
+3. The reduction of partial gradients fused with the SGD step and update equals the unfused
+   launches bit for bit (reduce_partial: proj/src/simulator.cpp:106-115; scale / sub:
+   proj/src/dense.cpp:183-191).
+"""
+import json
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+from tests.conftest import golden_stems, load_golden, normwise, stem_id
+
+pytestmark = pytest.mark.gpu
+
+STEMS = golden_stems()
+K12 = [s for s in STEMS if (".k1." in s or ".k2." in s) and stem_id(s).split(".")[0] in
+       ("cfg1_mlp3x1024_b64", "cfg2r_mlp5x256_b64", "fcr_alexnet_b32", "cnnr_train_b16", "mlp_train_d3",
+        "mlp_train_d2", "alexr_conv_b4", "cfg1_bf16", "mlp_train_d2_bf16", "reduce_kat", "wideconv_b2")]
+TOL_CHAIN_FP32 = 5e-2
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    assert torch.cuda.is_available(), "GPU test needs a CUDA device"
+    from paper_1805_04170_b200.executor import Context
+    return Context(0)
+
+
+def holders_after_step(ctx, text, P, seed, precision, flags, steps=1):
+    from paper_1805_04170_b200.executor import PlanExecutor
+    ex = PlanExecutor(ctx, text, precision=precision, flags=flags)
+    ex.init_inputs(seed)
+    for _ in range(steps):
+        ex.execute()
+    ex.synchronize()
+    out = {h: ex.read_node(h) for hs in P["holders"].values() for h in hs}
+    ex.close()
+    return out
+
+
+@pytest.mark.parametrize("stem", K12, ids=stem_id)
+def test_peer_self_matches_hbm_copy(ctx, stem):
+    from paper_1805_04170_b200.executor import FLAG_FORCE_XCHG, FLAG_FUSE, FLAG_GRAPH, FLAG_PEER, PREC_FP32, PREC_TF32
+    text, P, _, seed = load_golden(stem)
+    precs = [PREC_TF32] if "_bf16" in stem else [PREC_TF32, PREC_FP32]
+    for prec in precs:
+        want = holders_after_step(ctx, text, P, seed, prec, FLAG_FUSE)
+        for flags, steps in ((FLAG_FUSE | FLAG_FORCE_XCHG | FLAG_PEER, 1),
+                             (FLAG_FUSE | FLAG_FORCE_XCHG | FLAG_PEER | FLAG_GRAPH, 2)):
+            got = holders_after_step(ctx, text, P, seed, prec, flags, steps)
+            for h in want:
+                assert np.array_equal(got[h], want[h]), (stem, prec, flags, h)
+
+
+@pytest.mark.parametrize("stem", [s for s in K12 if stem_id(s).startswith(
+    ("mlp_train_d2.data", "mlp_train_d3.opt", "alexr_conv_b4.data.k1", "mlp_train_d2_bf16.data", "fcr_alexnet_b32.opt"))],
+    ids=stem_id)
+def test_fused_reduce_sgd_matches_unfused(ctx, stem):
+    """The reduction launch that also writes gw -> wd = lr*gw -> w_next = w - wd (or the tanh of a
+    reduced pre-activation) stores exactly what the separate launches store."""
+    from paper_1805_04170_b200.executor import FLAG_FUSE, PlanExecutor, PREC_FP32, PREC_TF32
+    text, P, _, seed = load_golden(stem)
+    prec = PREC_TF32 if "_bf16" in stem else PREC_FP32
+    ex = PlanExecutor(ctx, text, precision=prec, flags=FLAG_FUSE)
+    red = [s for s in ex.describe()["main"]["steps"] if s["kind"] == "nary" and s["what"] == "reduce"]
+    ex.close()
+    assert sum(s["chained"] for s in red) > 0, "no reduction carries a fused consumer"
+    fused = holders_after_step(ctx, text, P, seed, prec, FLAG_FUSE)
+    plain = holders_after_step(ctx, text, P, seed, prec, 0)
+    for h in fused:
+        assert np.array_equal(fused[h], plain[h]), h
+
+
+# ------------------------------------------------------------------ two ranks, one GPU
+TWO_RANK = [s for s in K12 if stem_id(s).startswith(
+    ("cfg1_mlp3x1024_b64.opt.k1", "cfg1_mlp3x1024_b64.data.k2", "cfg2r_mlp5x256_b64.opt.k2", "fcr_alexnet_b32.opt.k2",
+     "mlp_train_d3.hybrid.k2", "mlp_train_d2.data.k2", "alexr_conv_b4.opt.k1", "cnnr_train_b16.opt.k2",
+     "cfg1_bf16.opt.k1", "reduce_kat"))]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _peer_worker(rank, world, port, stems, outdir, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("TPX_PEER_TIMEOUT_S", "60")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1805_04170_b200.executor import (FLAG_FUSE, FLAG_GRAPH, FLAG_LOOP, FLAG_PEER, PREC_FP32,
+                                                    PREC_TF32, Context, PlanExecutor)
+        ctx = Context(0, rank, world)
+        for stem in stems:
+            text, P, _, seed = load_golden(stem)
+            prec = PREC_TF32 if "_bf16" in stem else PREC_FP32
+            for tag, flags, steps in (("eager", FLAG_FUSE | FLAG_PEER, 1), ("graph", FLAG_FUSE | FLAG_PEER | FLAG_GRAPH, 2),
+                                      ("loop", FLAG_FUSE | FLAG_PEER | FLAG_LOOP, 3),
+                                      ("carry", FLAG_FUSE | FLAG_PEER, 3)):
+                ex = PlanExecutor(ctx, text, precision=prec, flags=flags)
+                ex.connect_peers_from_torch()
+                ex.init_inputs(seed)
+                for i in range(steps):
+                    ex.execute()
+                    if tag == "carry" and i + 1 < steps:
+                        ex.carry_weights()
+                ex.synchronize()
+                mine = set(ex.my_devices())
+                vals = {}
+                for n in P["nodes"]:
+                    if n["device"] in mine:
+                        try:
+                            vals[n["id"]] = ex.read_node(n["id"])
+                        except Exception:  # pieces written into their concat / read in place
+                            pass
+                np.savez(os.path.join(outdir, f"{stem_id(stem)}.{tag}.r{rank}.npz"), **vals)
+                dist.barrier()  # no rank frees its arena while the other may still read it
+                ex.close()
+        dist.barrier()
+        q.put((rank, "ok", ""))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, "err", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(900)
+def test_two_ranks_on_one_gpu_peer_pull():
+    import torch.multiprocessing as mp
+    outdir = tempfile.mkdtemp(prefix="tpx_peer_")
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _free_port()
+    procs = [mpc.Process(target=_peer_worker, args=(r, 2, port, TWO_RANK, outdir, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(800)
+    res = [q.get(timeout=10) for _ in procs]
+    assert all(r[1] == "ok" for r in res), res
+    from oracle import tileplan_oracle as O
+    report = {}
+    for stem in TWO_RANK:
+        text, P, _, seed = load_golden(stem)
+        golden = O.execute_nodes(P, O.serial_execute(P["graph"], seed))
+        nodes = {n["id"]: n for n in P["nodes"]}
+        runs = {}
+        for tag in ("eager", "graph", "loop", "carry"):
+            v = {}
+            for r in range(2):
+                v.update(dict(np.load(os.path.join(outdir, f"{stem_id(stem)}.{tag}.r{r}.npz"))))
+            runs[tag] = v
+        eager = runs["eager"]
+        worst = 0.0
+        bf = "_bf16" in stem
+        for hs in P["holders"].values():
+            for h in hs:
+                if not bf:
+                    worst = max(worst, normwise(eager[h], golden[h]))
+                assert np.array_equal(runs["graph"][h], eager[h]), (stem, "graph", h)
+                assert np.all(np.isfinite(eager[h]))
+        # every fetched piece equals its source region (on whichever rank it lives) bit for bit
+        # (a piece pasted straight into its concat is checked at its place there)
+        consumer = {}
+        for n in P["nodes"]:
+            for src in n.get("sources", []):
+                consumer.setdefault(src, []).append(n)
+
+        def region_of(node_id, region):
+            m = nodes[node_id]
+            sl = tuple(slice(lo - m0, hi - m0) for (lo, hi), (m0, _) in zip(region, m["region"]))
+            return eager[node_id][sl]
+
+        pieces = 0
+        for n in P["nodes"]:
+            if n["kind"] != "fetch":
+                continue
+            s = nodes[n["sources"][0]]
+            if s["id"] not in eager:
+                continue
+            if n["id"] in eager:
+                got = eager[n["id"]]
+            else:
+                cats = [c for c in consumer.get(n["id"], []) if c["kind"] == "concat" and c["id"] in eager]
+                if not cats:
+                    continue  # read in place by a reduction (checked through its result)
+                got = region_of(cats[0]["id"], n["region"])
+            assert np.array_equal(got, region_of(s["id"], n["region"])), (stem, n["id"])
+            pieces += 1
+        # three loop-mode steps == three steps with an explicit carry in between (every tensor an
+        # op produces; a weight's own holder reads differently once the carry ran after the step)
+        produced = {o["output"] for o in P["graph"]["ops"]}
+        for t, hs in P["holders"].items():
+            if t not in produced:
+                continue
+            for h in hs:
+                assert np.array_equal(runs["loop"][h], runs["carry"][h]), (stem, "loop", h)
+        report[stem_id(stem)] = {"chained_normwise_fp32": worst, "pieces_checked": pieces}
+        if not bf:
+            assert worst <= TOL_CHAIN_FP32, (stem, worst)
+    os.makedirs(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out"), exist_ok=True)
+    with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out",
+                           "peer_two_rank.json"), "w") as f:
+        json.dump(report, f, indent=1, sort_keys=True)
+    for p in procs:
+        assert p.exitcode == 0
