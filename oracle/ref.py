@@ -25,10 +25,15 @@ def build(quiet: bool = True) -> bool:
     """Compile oracle/_ref from /root/reference if that tree exists (only in the build
     container).  Returns True when the library is present afterwards."""
     if os.path.isdir("/root/reference/proj/src"):
-        out = subprocess.run(["make", "-C", HERE, "-j8"], capture_output=True, text=True)
+        # the library, and INTEGRATION.md's reference-side adapter linked against libtpx.so
+        # (integration/*.cpp -> oracle/_ref/adapter_b200; needs the product library built first)
+        out = subprocess.run(["make", "-C", HERE, "-j8", "all", "adapter"], capture_output=True, text=True)
         if out.returncode != 0:
             raise RuntimeError("oracle/_ref build failed:\n" + out.stdout + out.stderr)
     return os.path.exists(LIB_PATH)
+
+
+ADAPTER = os.path.join(HERE, "_ref", "adapter_b200")
 
 
 def available() -> bool:

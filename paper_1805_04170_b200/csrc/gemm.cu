@@ -1322,7 +1322,7 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 14) g_split_chain = int(sbo) & 15;  // (14,n) 3xTF32 TMEM chains of n k-blocks
   if (lbo == 15) g_odepth = int(sbo);             // (15,n) epilogue operand ring depth n
   if (lbo == 16) g_min_stages = int(sbo);         // (16,n) keep >= n mainloop stages
-  if (lbo >= 1 && lbo <= 14) g_dbg_lbo = g_dbg_sbo = 0;
+  if (lbo >= 1 && lbo <= 16) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {

@@ -78,6 +78,13 @@ def test_single_rank_lowering_bytes(stem):
     assert st["rank_xrank_bytes_in"] == 0 and st["n_nccl_groups"] == 0
     assert d["per_op_fetch_bytes_in"] == O.per_op_bytes(P)
     assert d["per_phase_fetch_bytes_in"] == O.fetch_bytes_by_phase(P)
+    # ... and equal the reference's own simulate_traffic phase totals (simulator.cpp:11-49)
+    from oracle import ref
+    if ref.available():
+        t = ref.simulate_traffic(text)
+        assert {r["phase"]: r["bytes"] for r in t["phases"] if r["bytes"]} == \
+            {k: v for k, v in d["per_phase_fetch_bytes_in"].items() if v}
+        assert t["total_bytes"] == P["fetch_bytes_total"]
     assert st["gemm_flops"] == sum(
         2 * _mm_flops(P, n) for n in P["nodes"] if n["kind"] == "sub_op" and _is_mm(P, n))
     assert st["n_kernel_launches"] > 0
