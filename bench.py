@@ -442,7 +442,30 @@ def main():
         st["swapped"] = sum(len(x["swapped"]) for x in d)
         return st
 
-    def quick(mode, suffix, kk, prec, flags, steps):
+    def conversion_times(exs):
+        """Time-model parity: the planner's time model prices a phase at its
+        bytes over the link bandwidth (simulate_traffic, proj/src/simulator.cpp:40-47).  Here the
+        link of a one-GPU tiled run is HBM (a fetch reads and writes its bytes once), so the model
+        is est = sum over phases of 2 x bytes / HBM peak; measured = the device time of the
+        lowered conversion steps (copies / pulls / reductions / syncs; CUDA events per step,
+        graph replay off), median of 3 steps."""
+        conv = ("copy", "pull", "pack", "nccl", "reduce", "signal", "barrier")
+        runs = []
+        for _ in range(3):
+            t = 0.0
+            for ex in exs:
+                ex.enable_timing(True)
+                ex.execute()
+                steps = ex.describe()["main"]["steps"]
+                t += sum(ms for ms, st in zip(ex.last_step_times(), steps) if st.get("what") in conv)
+                ex.enable_timing(False)
+            runs.append(t)
+        est = sum(2.0 * v for ex in exs for v in ex.describe()["per_phase_fetch_bytes_in"].values()) / (hbm_peak * 1e9)
+        meas = statistics.median(runs) / 1e3
+        return {"est_seconds_hbm": est, "measured_conversion_seconds": meas,
+                "measured_over_model": meas / est if est else None}
+
+    def quick(mode, suffix, kk, prec, flags, steps, model=False):
         """A plan set timed alone (variants): warm-up, then `steps` loop steps."""
         exs, _ = load(mode, suffix, kk, prec, flags)
         try:
@@ -453,12 +476,16 @@ def main():
                 step()
             ms = max_over_ranks(timed(step, stream, steps, barrier))
             st = stats_of(exs)
+            tm = conversion_times(exs) if model and st["fetch_bytes_total"] else None
         finally:
             for ex in exs:
                 ex.close()
-        return {"value": batch * steps / (ms / 1e3), "ms_per_step": ms / steps,
-                "fetch_bytes_total": st["fetch_bytes_total"], "carry_bytes_per_step": st["carry_bytes"],
-                "launches_per_step": st["n_kernel_launches"] + st["carry_launches"]}
+        r = {"value": batch * steps / (ms / 1e3), "ms_per_step": ms / steps,
+             "fetch_bytes_total": st["fetch_bytes_total"], "carry_bytes_per_step": st["carry_bytes"],
+             "launches_per_step": st["n_kernel_launches"] + st["carry_launches"]}
+        if tm:
+            r["time_model"] = tm
+        return r
 
     def measure(mode, suffix, prec):
         """One plan set (every component of the workload) timed end to end."""
@@ -634,7 +661,7 @@ def main():
                     if need > 0.85 * free:
                         row[label] = {"skipped": f"arena {need / 2**30:.1f} GiB > 85% of free HBM"}
                         continue
-                    row[label] = quick(mode, suffix, kk, prec, flags, vsteps)
+                    row[label] = quick(mode, suffix, kk, prec, flags, vsteps, model=label in ("opt_step_only", "data"))
                 if "data" in row and "value" in row["data"]:
                     for lab in ("opt", "opt_step_only", "loop", "loop_peer_path"):
                         if "value" in row.get(lab, {}):

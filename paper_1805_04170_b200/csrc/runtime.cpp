@@ -7,6 +7,8 @@
 #include <sstream>
 #include <tuple>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "json.h"
 #include "nccl_shim.h"
 #include "util.h"
@@ -1404,7 +1406,27 @@ void check_peer_error(PlanRt& P) {
   }
 }
 
+// NVTX range per lowered step, named "<op>:<what>" (the plan phase's op and the step's role):
+// visible in ncu / nsys timelines (header-only NVTX 3; inert unless a tool is attached).
+// TPX_NVTX=0 turns the ranges off.
+static bool nvtx_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("TPX_NVTX");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static void launch_step(PlanRt& P, Program& prog, const Step& s, cudaStream_t st) {
+  struct Range {
+    bool on;
+    explicit Range(const Step& s) : on(nvtx_on()) {
+      if (on) nvtxRangePushA((s.op.empty() ? s.what : s.op + ":" + s.what).c_str());
+    }
+    ~Range() {
+      if (on) nvtxRangePop();
+    }
+  } range(s);
   switch (s.kind) {
     case ST_NARY: nary_run(prog.nary[size_t(s.idx)], st); break;
     case ST_GEMM: gemm_run(prog.gemm[size_t(s.idx)], st); break;

@@ -267,11 +267,15 @@ def execute_numeric(plan_json: str, seed: int, ctx: Optional[Context] = None,
                     precision: int = PREC_TF32, flags: int = FLAG_FUSE) -> NumericCheck:
     """B200 counterpart of execute_numeric (simulator.cpp:55-149): the tiled plan and the
     single-device run both execute on this GPU; every holder block of every tensor on every
-    device is compared."""
+    device is compared.  Multi-rank (ctx.world > 1): each rank checks the holders of its own
+    logical devices; the single-device truth runs on a world-1 context of the same GPU."""
     ctx = ctx or Context(0)
     plan = json.loads(plan_json)
     tiled = PlanExecutor(ctx, plan_json, precision, flags)
-    serial = PlanExecutor(ctx, serial_plan(plan["graph"]), precision, flags)
+    if ctx.world > 1 and (flags & FLAG_PEER):
+        tiled.connect_peers_from_torch()
+    solo = ctx if ctx.world == 1 else Context(ctx.ordinal, 0, 1)
+    serial = PlanExecutor(solo, serial_plan(plan["graph"]), precision, flags & ~(FLAG_PEER | FLAG_FORCE_XCHG))
     tiled.init_inputs(seed)
     serial.init_inputs(seed)
     tiled.execute()

@@ -68,7 +68,7 @@ def test_gemm_act_epilogue_bitexact():
 
 @pytest.mark.parametrize("shape,epi", [((1024, 4096, 256, True, False), [3, 6]), ((512, 1024, 1024, False, True), [1]),
                                        ((64, 1024, 1024, False, False), None), ((1000, 136, 72, True, True), None)],
-                         ids=["pair_update", "pair_act", "small", "edge"])
+                         ids=["tn_update", "nt_act", "small", "edge"])  # (pair kernels: test_gpu_fullsize.py)
 def test_gemm_dynamic_schedule(shape, epi):
     """Whole-tile schedules handed out by the device tile counter (debug knob (10, 0)):
     same results as the static per-CTA lists, twice in a row (the counter re-arms itself)."""

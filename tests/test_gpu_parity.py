@@ -6,7 +6,7 @@ tests/test_oracle.py) supplies every node's fp64 value.  Two checks per plan (SU
 * per-op, teacher-forced: the oracle's values are written into the op's input holders, only
   that op's lowered steps run, and every output holder block is compared.  Stated tolerance
   (normwise max|d| / max|ref| per block):
-      PREC_FP32 (3xTF32 split, fp32-accurate products)   <= 1e-5
+      PREC_FP32 (3xTF32 split, fp32-accurate products)   <= 2e-6  (measured <= 9.0e-7)
       PREC_TF32 (single-pass kind::tf32, fp32 accumulate) <= 2e-3
 * bf16 plans (graph dtype_bytes 2, "_bf16" stems): bf16 storage, kind::f16 products with
   fp32 accumulation, every stored value rounded to bf16.  Per-op teacher-forced gate
@@ -15,11 +15,13 @@ tests/test_oracle.py) supplies every node's fp64 value.  Two checks per plan (SU
   of max|ref|).  Chained values are checked finite and reported, not gated.
 * chained: the whole step from seeded inputs.  The reference's op semantics make the
   backward chain ill-conditioned (dact = 1 - tanh^2(h) on unscaled U[-1,1) inits), so the
-  chained gate applies to the fp32-accurate path only: <= 5e-2 normwise on every holder;
+  chained gate applies to the fp32-accurate path only: <= 2e-2 normwise on every holder (SURVEY
+  §7 H5: ~2x the fp32 floor; measured <= 7.5e-3);
   TF32 chained errors are reported in the profiles, not gated.
 Inputs are bit-exact: seeded_tensor is generated on device (fp64 -> fp32 round to nearest).
 """
 import json
+import os
 
 import numpy as np
 import pytest
@@ -30,9 +32,9 @@ from tests.conftest import golden_stems, load_golden, normwise, stem_id
 pytestmark = pytest.mark.gpu
 
 STEMS = golden_stems()
-TOL_OP = {1: 1e-5, 0: 2e-3}
+TOL_OP = {1: 2e-6, 0: 2e-3}
 TOL_OP_BF16 = 1e-2
-TOL_CHAIN_FP32 = 5e-2
+TOL_CHAIN_FP32 = 2e-2
 
 
 def is_bf16(stem):
@@ -48,6 +50,20 @@ def ctx():
 
 
 _cache = {}
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+
+
+def _record(kind, stem, value, where):
+    """Measured errors of every golden plan, kept for the profiles (gpurun_out/parity_golden.json)."""
+    os.makedirs(OUT, exist_ok=True)
+    path = os.path.join(OUT, "parity_golden.json")
+    d = {}
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+    d.setdefault(kind, {})[stem_id(stem)] = [value, where]
+    with open(path, "w") as f:
+        json.dump(d, f, indent=1, sort_keys=True)
 
 
 def oracle_values(stem):
@@ -101,6 +117,7 @@ def test_per_op_fp32(ctx, stem):
     if is_bf16(stem):
         pytest.skip("3xTF32 is an fp32-storage mode")
     e, op = run_per_op(ctx, stem, 1)
+    _record("per_op_fp32", stem, e, op)
     assert e <= TOL_OP[1], (op, e)
 
 
@@ -108,6 +125,7 @@ def test_per_op_fp32(ctx, stem):
 def test_per_op_tf32(ctx, stem):
     """TF32 products on fp32 plans; bf16 products and storage on bf16 plans."""
     e, op = run_per_op(ctx, stem, 0)
+    _record("per_op_bf16" if is_bf16(stem) else "per_op_tf32", stem, e, op)
     assert e <= (TOL_OP_BF16 if is_bf16(stem) else TOL_OP[0]), (op, e)
 
 
@@ -115,9 +133,11 @@ def test_per_op_tf32(ctx, stem):
 def test_chained_fp32(ctx, stem):
     if is_bf16(stem):
         e, t = run_chained(ctx, stem, 0)
+        _record("chained_bf16", stem, e, t)
         assert np.isfinite(e), (t, e)  # bf16 chained error: reported, not gated
         return
     e, t = run_chained(ctx, stem, 1)
+    _record("chained_fp32", stem, e, t)
     assert e <= TOL_CHAIN_FP32, (t, e)
 
 
