@@ -367,10 +367,10 @@ def main():
                     help="N > 1 cross-rank fetches: peer pulls over NVLink (CUDA IPC) or NCCL send/recv")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch(args))  # one process per GPU (both arms launch the same way)
     if args.impl == "reference":
         return run_reference(args)
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        raise SystemExit(relaunch(args))
 
     import torch
     import torch.distributed as dist
@@ -385,11 +385,22 @@ def main():
     k = int(round(math.log2(world)))
     if 1 << k != world or k > 3:
         raise SystemExit("N must be 1, 2, 4 or 8")
+    # TPX_BENCH_SHARE_GPU=1: every rank on cuda:0 (exercises the N > 1 code path -- peer pulls
+    # between processes, counters, barriers -- on a one-GPU box; its numbers are not scaling data)
+    share = os.environ.get("TPX_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if torch.cuda.device_count() < world and world > 1 and local >= torch.cuda.device_count():
         raise SystemExit(f"--gpus {world} needs {world} GPUs; this node has {torch.cuda.device_count()}")
     torch.cuda.set_device(local)
+    peer = world > 1 and args.xchg == "peer"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # peer mode moves no data through torch.distributed (only IPC handles, barriers and the
+        # max over ranks of the device times), so gloo suffices; NCCL mode needs the NCCL group
+        if peer:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -398,7 +409,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if peer else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
@@ -406,7 +417,6 @@ def main():
     batch = workload_batch(args.config)
     prec = 1 if args.precision == "fp32" else 0  # bf16: storage type comes from the bf16 plan
     ctx = Context(local, rank, world)
-    peer = world > 1 and args.xchg == "peer"
     if world > 1 and not peer:
         ctx.init_comm_from_torch()
         print(f"[bench] rank {rank}: NCCL communicator initialised (nranks={world}, device cuda:{local})",
@@ -617,7 +627,7 @@ def main():
             e2e_step()
         stream.wait_stream(copy)
         e_ms = max_over_ranks(timed_once(e2e_run, stream, barrier))
-        tot = torch.tensor([h2d, d2h], dtype=torch.float64, device="cuda")
+        tot = torch.tensor([h2d, d2h], dtype=torch.float64, device="cpu" if peer else "cuda")
         if world > 1:
             dist.all_reduce(tot)
         r["e2e"] = {"value": batch * args.steps / (e_ms / 1e3), "unit": "samples/s",

@@ -86,23 +86,30 @@ __device__ __forceinline__ int find_desc(const int64_t* tile_begin_base, size_t 
   return lo;
 }
 
-// Row tiling shared by nary / init: rows x inner (units) split into tiles of ~kTileUnits.
+// Row tiling shared by nary / init: rows x inner (units) split into tiles of ~`tile` units.  A
+// tile is either a chunk of one long row (all threads on it) or rpt whole rows walked by groups
+// of rg threads (rg = 32..256, about 4 units per thread per row, so short rows still keep every
+// thread busy).
 struct RowTiling {
-  int64_t rows, inner, rpt, col_chunk, n_col_chunks;
+  int64_t rows, inner, rpt, col_chunk, n_col_chunks, rg;
 };
 
-RowTiling row_tiling(int64_t rows, int64_t inner) {
+RowTiling row_tiling(int64_t rows, int64_t inner, int64_t tile = kTileUnits) {
   RowTiling t;
   t.rows = rows;
   t.inner = inner;
-  if (inner >= kTileUnits) {
+  if (inner >= tile) {
     t.rpt = 1;
-    t.col_chunk = kTileUnits;
-    t.n_col_chunks = (inner + kTileUnits - 1) / kTileUnits;
+    t.col_chunk = tile;
+    t.n_col_chunks = (inner + tile - 1) / tile;
+    t.rg = kThreads;
   } else {
-    t.rpt = std::max<int64_t>(1, kTileUnits / std::max<int64_t>(inner, 1));
-    t.col_chunk = inner;
+    t.col_chunk = std::max<int64_t>(inner, 1);
     t.n_col_chunks = 1;
+    int64_t rg = 32;
+    while (rg < kThreads && rg * 4 < inner) rg *= 2;
+    t.rg = rg;
+    t.rpt = std::max<int64_t>(kThreads / rg, tile / t.col_chunk);
   }
   return t;
 }
@@ -111,7 +118,7 @@ RowTiling row_tiling(int64_t rows, int64_t inner) {
 
 struct NaryDev {
   NaryDesc d;
-  int64_t rows, inner, rpt, col_chunk, n_col_chunks;
+  int64_t rows, inner, rpt, col_chunk, n_col_chunks, rg;
 };
 
 __device__ __forceinline__ float nary_apply(int op, int nin, const float* v, float s) {
@@ -149,21 +156,25 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 // Wait until every rank in `mask` has reached count `c` (bounded: a wait that outlives
 // timeout_ns records the rank in the host-mapped error word and gives up instead of hanging).
-__device__ void peer_wait(const PeerSync& s, uint32_t mask, unsigned long long c) {
-  for (int r = 0; r < s.world; ++r) {
-    if (!(mask >> r & 1u)) continue;
-    const unsigned long long* p = s.peer[r];
-    if (ld_acquire_sys(p) >= c) continue;
-    const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(p) < c) {
-      if (*reinterpret_cast<volatile int*>(s.err)) return;
-      __nanosleep(200);
-      if (globaltimer() - t0 > s.timeout_ns) {
-        atomicExch(s.err, 0x100 | r);
-        return;
-      }
+__device__ __forceinline__ bool peer_wait_one(const unsigned long long* p, unsigned long long c, int* err,
+                                              unsigned long long timeout_ns, int r) {
+  if (ld_acquire_sys(p) >= c) return true;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys(p) < c) {
+    if (*reinterpret_cast<volatile int*>(err)) return false;
+    __nanosleep(200);
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicExch(err, 0x100 | r);
+      return false;
     }
   }
+  return true;
+}
+// (ranks unrolled: the counters stay in the kernel's parameter space, no local copy)
+__device__ __forceinline__ void peer_wait(const PeerSync& s, uint32_t mask, unsigned long long c) {
+#pragma unroll
+  for (int r = 0; r < kMaxRanks; ++r)
+    if ((mask >> r & 1u) && !peer_wait_one(s.peer[r], c, s.err, s.timeout_ns, r)) return;
 }
 
 __global__ void sync_kernel(PeerSync s, int barrier) {
@@ -193,10 +204,21 @@ __device__ __forceinline__ float stored(float v) {
   else return v;
 }
 
+// The block's descriptor, staged in shared memory once (a per-thread walk of the global
+// descriptor table costs dozens of dependent loads per block).
 template <class T>
-__global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restrict__ ds, int n, PeerSync sync) {
-  const int di = find_desc(&ds[0].d.tile_begin, sizeof(NaryDev), n, blockIdx.x);
-  const NaryDev& D = ds[di];
+__global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __restrict__ ds, int n, PeerSync sync) {
+  __shared__ __align__(16) unsigned char sraw[(sizeof(NaryDev) + 15) / 16 * 16];
+  __shared__ int sdi;
+  if (threadIdx.x == 0) sdi = find_desc(&ds[0].d.tile_begin, sizeof(NaryDev), n, blockIdx.x);
+  __syncthreads();
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(ds + sdi);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(sraw);
+    for (int i = threadIdx.x; i < int(sizeof(NaryDev) / 4); i += kThreads) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  const NaryDev& D = *reinterpret_cast<const NaryDev*>(sraw);
   const NaryDesc& d = D.d;
   if (d.wait_mask) {  // peer pull: the sources on other ranks must be complete
     if (threadIdx.x == 0) peer_wait(sync, d.wait_mask, *sync.local);
@@ -207,11 +229,11 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
   const int64_t r0 = rb * D.rpt, r1 = min(D.rows, r0 + D.rpt);
   const int64_t c0 = cc * D.col_chunk, c1 = min(D.inner, c0 + D.col_chunk);
   const int nin = d.nin, op = d.op, nch = d.n_chain;
-  // one row per warp; a block holding a single (long) row spreads it over all its threads
-  const bool one = (r1 - r0) == 1;
-  const int warp = one ? 0 : int(threadIdx.x >> 5), lane = one ? int(threadIdx.x) : int(threadIdx.x & 31);
-  const int cstep = one ? kThreads : 32;
-  for (int64_t r = r0 + warp; r < r1; r += kThreads / 32) {
+  // groups of rg threads walk the tile's rows (rg = kThreads: one row chunk, all threads on it)
+  const int rg = int(D.rg);
+  const int warp = int(threadIdx.x) / rg, lane = int(threadIdx.x) % rg;
+  const int cstep = rg;
+  for (int64_t r = r0 + warp; r < r1; r += kThreads / rg) {
     const int64_t i2 = r % d.shape[2];
     const int64_t t = r / d.shape[2];
     const int64_t i1 = t % d.shape[1];
@@ -282,11 +304,72 @@ __global__ void __launch_bounds__(kThreads) nary_kernel(const NaryDev* __restric
   }
 }
 
+// Batches made only of plain box copies (pack / unpack / pull / concat pieces, no chain): one
+// source per descriptor, so a light kernel (few registers, full occupancy) with 8 independent
+// loads in flight per thread -- enough to cover NVLink latency on a peer read.
+template <class T>
+__global__ void __launch_bounds__(kThreads, 3) copy_kernel(const NaryDev* __restrict__ ds, int n, PeerSync sync) {
+  __shared__ int sdi;
+  if (threadIdx.x == 0) {
+    const int di = find_desc(&ds[0].d.tile_begin, sizeof(NaryDev), n, blockIdx.x);
+    sdi = di;
+    if (ds[di].d.wait_mask) peer_wait(sync, ds[di].d.wait_mask, *sync.local);
+  }
+  __syncthreads();
+  const NaryDev& D = ds[sdi];
+  const int64_t tb = D.d.tile_begin, nch = D.n_col_chunks, rpt = D.rpt, rows = D.rows, inner = D.inner;
+  const int64_t colc = D.col_chunk;
+  const int64_t sh1 = D.d.shape[1], sh2 = D.d.shape[2];
+  const int64_t o0 = D.d.out_st[0], o1 = D.d.out_st[1], o2 = D.d.out_st[2], o3 = D.d.out_st[3];
+  const int64_t s0 = D.d.in_st[0][0], s1 = D.d.in_st[0][1], s2 = D.d.in_st[0][2], s3 = D.d.in_st[0][3];
+  const int vec = D.d.vec;
+  T* const obase = reinterpret_cast<T*>(D.d.out);
+  const T* const ibase = reinterpret_cast<const T*>(D.d.in[0]);
+  const int64_t local = int64_t(blockIdx.x) - tb;
+  const int64_t rb = local / nch, cc = local % nch;
+  const int64_t r0 = rb * rpt, r1 = min(rows, r0 + rpt);
+  const int64_t c0 = cc * colc, c1 = min(inner, c0 + colc);
+  const int rg = int(D.rg);
+  const int warp = int(threadIdx.x) / rg, lane = int(threadIdx.x) % rg;
+  const int cstep = rg;
+  constexpr int U = 8;
+  for (int64_t r = r0 + warp; r < r1; r += kThreads / rg) {
+    const int64_t i2 = r % sh2;
+    const int64_t t = r / sh2;
+    const int64_t i1 = t % sh1;
+    const int64_t i0 = t / sh1;
+    T* out = obase + i0 * o0 + i1 * o1 + i2 * o2;
+    const T* src = ibase + i0 * s0 + i1 * s1 + i2 * s2;
+    if (vec == 4) {
+      for (int64_t cb = c0 + lane; cb < c1; cb += U * cstep) {
+        float4 v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (cb + j * cstep < c1) v[j] = eld4(src + 4 * (cb + j * cstep));
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (cb + j * cstep < c1) est4(out + 4 * (cb + j * cstep), v[j]);
+      }
+    } else {
+      constexpr int U1 = 4;
+      for (int64_t cb = c0 + lane; cb < c1; cb += U1 * cstep) {
+        float v[U1];
+#pragma unroll
+        for (int j = 0; j < U1; ++j)
+          if (cb + j * cstep < c1) v[j] = eld(src + (cb + j * cstep) * s3);
+#pragma unroll
+        for (int j = 0; j < U1; ++j)
+          if (cb + j * cstep < c1) est(out + (cb + j * cstep) * o3, v[j]);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- init (seeded_tensor)
 
 struct InitDev {
   InitDesc d;
-  int64_t rows, inner, rpt, col_chunk, n_col_chunks;
+  int64_t rows, inner, rpt, col_chunk, n_col_chunks, rg;
 };
 
 __device__ __forceinline__ float seeded_value(uint64_t state0, uint64_t flat) {
@@ -309,8 +392,11 @@ __global__ void __launch_bounds__(kThreads) init_kernel(const InitDev* __restric
   const int64_t rb = local / D.n_col_chunks, cc = local % D.n_col_chunks;
   const int64_t r0 = rb * D.rpt, r1 = min(D.rows, r0 + D.rpt);
   const int64_t c0 = cc * D.col_chunk, c1 = min(D.inner, c0 + D.col_chunk);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t r = r0 + warp; r < r1; r += kThreads / 32) {
+  // groups of rg threads walk the tile's rows (rg = kThreads: one row chunk, all threads on it)
+  const int rg = int(D.rg);
+  const int warp = int(threadIdx.x) / rg, lane = int(threadIdx.x) % rg;
+  const int cstep = rg;
+  for (int64_t r = r0 + warp; r < r1; r += kThreads / rg) {
     const int64_t i2 = r % d.ext[2];
     const int64_t t = r / d.ext[2];
     const int64_t i1 = t % d.ext[1];
@@ -320,7 +406,7 @@ __global__ void __launch_bounds__(kThreads) init_kernel(const InitDev* __restric
          uint64_t(d.lo[2] + i2)) * d.full[3] + uint64_t(d.lo[3]);
     T* out = reinterpret_cast<T*>(d.out) + r * d.ext[3];
     // fp64 -> fp32 (round to nearest) -> storage type (bf16: round to nearest even)
-    for (int64_t c = c0 + lane; c < c1; c += 32) est(out + c, seeded_value(d.state0, rowflat + uint64_t(c)));
+    for (int64_t c = c0 + lane; c < c1; c += cstep) est(out + c, seeded_value(d.state0, rowflat + uint64_t(c)));
   }
 }
 
@@ -684,27 +770,45 @@ NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView
 
 void nary_prepare(NaryBatch& b) {
   std::vector<NaryDev> dev(b.descs.size());
+  // tile size: as large as kTileUnits while the batch still gives >= ~8 blocks per SM, smaller
+  // for small batches (a 4 MB strided copy should not run on 32 blocks)
+  int64_t total = 0;
+  for (const auto& d : b.descs) total += d.units;
+  int64_t tile = kTileUnits;
+  while (tile > 1024 && total / tile < 8 * 148) tile /= 2;
   int64_t tiles = 0;
   b.bytes = 0;
   for (size_t i = 0; i < b.descs.size(); ++i) {
     NaryDesc& d = b.descs[i];
     const int64_t rows = d.shape[0] * d.shape[1] * d.shape[2];
     const int64_t inner = d.shape[3] / d.vec;
-    RowTiling t = row_tiling(rows, inner);
+    RowTiling t = row_tiling(rows, inner, tile);
     d.tile_begin = tiles;
     tiles += ((rows + t.rpt - 1) / t.rpt) * t.n_col_chunks;
-    dev[i] = NaryDev{d, t.rows, t.inner, t.rpt, t.col_chunk, t.n_col_chunks};
+    dev[i] = NaryDev{d, t.rows, t.inner, t.rpt, t.col_chunk, t.n_col_chunks, t.rg};
     const double elems = double(d.units) * d.vec;
     int streams = d.nin + 1 + (d.op == NARY_ACC ? 1 : 0);
     for (int c = 0; c < d.n_chain; ++c) streams += 1 + (d.chain[c].other ? 1 : 0);
     b.bytes += (b.bf16 ? 2.0 : 4.0) * elems * streams;
   }
   b.tiles = tiles;
+  b.copy_only = true;
+  for (const auto& d : b.descs) b.copy_only = b.copy_only && d.op == NARY_COPY && d.n_chain == 0;
   upload(dev, &b.d_descs);
 }
 
 void nary_run(const NaryBatch& b, cudaStream_t s) {
   if (!b.tiles) return;
+  if (b.copy_only) {
+    if (b.bf16)
+      copy_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
+                                                                        int(b.descs.size()), b.sync);
+    else
+      copy_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
+                                                                int(b.descs.size()), b.sync);
+    CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   if (b.bf16)
     nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
                                                                       int(b.descs.size()), b.sync);
@@ -766,7 +870,7 @@ void init_prepare(InitBatch& b) {
     RowTiling t = row_tiling(rows, d.ext[3]);
     d.tile_begin = tiles;
     tiles += ((rows + t.rpt - 1) / t.rpt) * t.n_col_chunks;
-    dev[i] = InitDev{d, t.rows, t.inner, t.rpt, t.col_chunk, t.n_col_chunks};
+    dev[i] = InitDev{d, t.rows, t.inner, t.rpt, t.col_chunk, t.n_col_chunks, t.rg};
   }
   b.tiles = tiles;
   upload(dev, &b.d_descs);

@@ -90,6 +90,7 @@ void sync_signal(const PeerSync& s, bool barrier, cudaStream_t st);
 struct NaryBatch {
   bool bf16 = false;  // storage type of every operand (arithmetic is fp32)
   bool pull = false;  // some descriptor reads peer memory (waits on PeerSync first)
+  bool copy_only = false;  // every descriptor a plain copy: the light copy kernel (nary_prepare)
   PeerSync sync;
   std::vector<NaryDesc> descs;
   void* d_descs = nullptr;
