@@ -2,6 +2,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+
+#include <algorithm>
 #include <cstring>
 #include <vector>
 #include <string>
@@ -68,6 +71,7 @@ __attribute__((visibility("default"))) int tpx_gemm_timed(
     int dev = 0, sms = 148;
     CUDA_CHECK(cudaGetDevice(&dev));
     CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (const char* cap = std::getenv("TPX_GEMM_SMS")) sms = std::max(2, std::min(sms, std::atoi(cap)));  // debug
     tpx::GemmLaunch g = tpx::gemm_prepare({s}, sms, precision == 1);  // 2: bf16 storage (GemmSpec.bf16)
     record_launch(g);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
