@@ -1221,6 +1221,7 @@ int g_split_chain = 2; // 3xTF32: k-blocks per TMEM accumulation chain (debug (1
 bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-in (10,0)
 int g_odepth = 0;      // debug (15, n): operand ring depth n (0 = chosen from the smem budget)
 int g_min_stages = 4;  // debug (16, n): mainloop stages the operand ring must leave
+int g_ts_chain = 0;    // debug (18, n): TMA-store epilogue also for chains (n = 1 single, 2 double-buffered boxes)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1322,7 +1323,8 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 14) g_split_chain = int(sbo) & 15;  // (14,n) 3xTF32 TMEM chains of n k-blocks
   if (lbo == 15) g_odepth = int(sbo);             // (15,n) epilogue operand ring depth n
   if (lbo == 16) g_min_stages = int(sbo);         // (16,n) keep >= n mainloop stages
-  if (lbo >= 1 && lbo <= 16) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
+  if (lbo == 18) g_ts_chain = int(sbo);           // (18,n) TMA-store chain epilogues
+  if (lbo >= 1 && lbo <= 18) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1612,7 +1614,7 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     // TMA-store epilogue for a lone row-major, 16-byte-pitched output (measured: faster for
     // plain products, e.g. the conv grad_input columns; slower than the per-lane stores when a
     // chain of stages shares the epilogue smem with the operand ring)
-    bool ts = !g_no_tma_out && s.n_epi == 0;
+    bool ts = !g_no_tma_out && (s.n_epi == 0 || g_ts_chain > 0);
     for (int e = 0; e <= s.n_epi; ++e) {
       const float* b = e == 0 ? pr.out : pr.epi[e - 1].out;
       const long long rs = e == 0 ? pr.out_rs : pr.epi[e - 1].out_rs, cs = e == 0 ? pr.out_cs : pr.epi[e - 1].out_cs;
@@ -1627,7 +1629,8 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
         store_idx.push_back({int(i), e});
       }
       pr.tstore = 1;
-      g.nbox = std::max(g.nbox, 2 * (1 + s.n_epi));  // double-buffered boxes
+      const int bufs = (s.n_epi > 0 && (g_ts_chain == 1 || 2 * (1 + s.n_epi) > 7)) ? 1 : 2;  // (NBOX: 3 bits)
+      g.nbox = std::max(g.nbox, bufs * (1 + s.n_epi));  // (double-buffered) boxes
     }
     auto small = [](long long x) { return x >= 0 && x < (1ll << 31); };
     bool ok = small(pr.out_rs) && small(pr.out_cs);

@@ -148,30 +148,40 @@ def _peer_worker(rank, world, port, stems, outdir, q):
         dist.destroy_process_group()
 
 
+FOUR_RANK = [s for s in STEMS if stem_id(s).startswith(
+    ("cfg1_mlp3x1024_b64.opt.k2", "cfg2r_mlp5x256_b64.opt.k3", "mlp_train_d3.hybrid.k2", "fcr_alexnet_b32.opt.k3",
+     "mlp_train_d2.data.k2"))]
+
+
 @pytest.mark.timeout(900)
-def test_two_ranks_on_one_gpu_peer_pull():
+@pytest.mark.parametrize("world", [2, 4])
+def test_ranks_on_one_gpu_peer_pull(world):
+    """world 2 on k = 1..2 plans (each rank one or two logical devices), world 4 on k = 2..3 plans
+    (each rank one or two logical devices; 4 processes time-slice the GPU)."""
     import torch.multiprocessing as mp
+    stems = TWO_RANK if world == 2 else FOUR_RANK
     outdir = tempfile.mkdtemp(prefix="tpx_peer_")
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
     port = _free_port()
-    procs = [mpc.Process(target=_peer_worker, args=(r, 2, port, TWO_RANK, outdir, q)) for r in range(2)]
+    procs = [mpc.Process(target=_peer_worker, args=(r, world, port, stems, outdir, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(800)
     res = [q.get(timeout=10) for _ in procs]
+    assert len(stems) >= 4
     assert all(r[1] == "ok" for r in res), res
     from oracle import tileplan_oracle as O
     report = {}
-    for stem in TWO_RANK:
+    for stem in stems:
         text, P, _, seed = load_golden(stem)
         golden = O.execute_nodes(P, O.serial_execute(P["graph"], seed))
         nodes = {n["id"]: n for n in P["nodes"]}
         runs = {}
         for tag in ("eager", "graph", "loop", "carry"):
             v = {}
-            for r in range(2):
+            for r in range(world):
                 v.update(dict(np.load(os.path.join(outdir, f"{stem_id(stem)}.{tag}.r{r}.npz"))))
             runs[tag] = v
         eager = runs["eager"]
@@ -224,7 +234,30 @@ def test_two_ranks_on_one_gpu_peer_pull():
             assert worst <= TOL_CHAIN_FP32, (stem, worst)
     os.makedirs(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out"), exist_ok=True)
     with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out",
-                           "peer_two_rank.json"), "w") as f:
+                           f"peer_{world}_rank.json"), "w") as f:
         json.dump(report, f, indent=1, sort_keys=True)
     for p in procs:
         assert p.exitcode == 0
+
+
+@pytest.mark.timeout(900)
+def test_bench_two_ranks_on_one_gpu():
+    """bench.py's N = 2 path end to end (self-launch, peer arenas, device counters, max over
+    ranks, e2e) with both ranks on cuda:0 (TPX_BENCH_SHARE_GPU=1; the numbers are not scaling
+    data, the path is what is checked)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["TPX_BENCH_SHARE_GPU"] = "1"
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2",
+                          "--warmup", "3", "--no-variants", "--no-cpu-baseline", "--config", "cfg1_mlp3x1024_b64"],
+                         capture_output=True, text=True, timeout=800, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert "peer pull" in d["config"]["exchange"]
+    assert d["fetch_bytes_total"] > 0  # k = 1: the plan really crosses the rank boundary
+    assert out.stderr.count("peer arenas of 2 ranks mapped") == 2

@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1805_04170_b200 import native  # noqa: E402
 from tools.gemm_check import bench  # noqa: E402
 
-DEFAULTS = {4: 0, 10: 1, 11: 0, 12: 1, 15: 0, 16: 4, 5: 1, 7: 0, 8: 0}
+DEFAULTS = {4: 0, 10: 1, 11: 0, 12: 1, 15: 0, 16: 4, 5: 1, 7: 0, 8: 0, 18: 0}
 SHAPES = [("bwd_w+sgd tf32", (8192, 8192, 512, True, False), [3, 6], 0),
           ("bwd_w+sgd bf16", (8192, 8192, 512, True, False), [3, 6], 2),
           ("fwd+act tf32", (512, 8192, 8192, False, False), [1], 0),

@@ -40,9 +40,10 @@ def main():
     en = load("fullsize_every_node.json")
     if en:
         out["fullsize_every_node_worst"] = en
-    pr = load("peer_two_rank.json")
-    if pr:
-        out["two_ranks_one_gpu_peer"] = pr
+    for w in (2, 4):
+        pr = load(f"peer_{w}_rank.json")
+        if pr:
+            out[f"peer_{w}_ranks_one_gpu"] = pr
     path = os.path.join(ROOT, "profiles", "r2_parity_fullsize.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
