@@ -207,10 +207,11 @@ __device__ __forceinline__ float stored(float v) {
 // The block's descriptor, staged in shared memory once (a per-thread walk of the global
 // descriptor table costs dozens of dependent loads per block).
 template <class T>
-__global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __restrict__ ds, int n, PeerSync sync) {
+__global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
+                                                           PeerSync sync) {
   __shared__ __align__(16) unsigned char sraw[(sizeof(NaryDev) + 15) / 16 * 16];
   __shared__ int sdi;
-  if (threadIdx.x == 0) sdi = find_desc(&ds[0].d.tile_begin, sizeof(NaryDev), n, blockIdx.x);
+  if (threadIdx.x == 0) sdi = __ldg(tile_desc + blockIdx.x);
   __syncthreads();
   {
     const uint32_t* src = reinterpret_cast<const uint32_t*>(ds + sdi);
@@ -244,6 +245,46 @@ __global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __rest
 #pragma unroll
     for (int k = 0; k < kMaxIn; ++k)
       if (k < nin) in[k] = reinterpret_cast<const T*>(d.in[k]) + i0 * d.in_st[k][0] + i1 * d.in_st[k][1] + i2 * d.in_st[k][2];
+    if (d.vec == 4 && op == NARY_SUM && nin <= 4) {
+      // partial-sum reduction (reduce_partial, <= 4 partials): 4 elements per thread in flight,
+      // summed left to right exactly like NARY_SUM, then the chained stages
+      constexpr int U = 4;
+      for (int64_t cb = c0 + lane; cb < c1; cb += U * cstep) {
+        float4 acc[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (cb + j * cstep < c1) acc[j] = eld4(in[0] + 4 * (cb + j * cstep));
+#pragma unroll
+        for (int k = 1; k < 4; ++k) {
+          if (k >= nin) break;
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+            if (cb + j * cstep < c1) {
+              const float4 v = eld4(in[k] + 4 * (cb + j * cstep));
+              acc[j].x += v.x; acc[j].y += v.y; acc[j].z += v.z; acc[j].w += v.w;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int64_t c = cb + j * cstep;
+          if (c >= c1) break;
+          float4 o = acc[j];
+          est4(out + 4 * c, o);
+          for (int s = 0; s < nch; ++s) {
+            const ChainStage& cs = d.chain[s];
+            const int64_t e = ooff + 4 * c;
+            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (cs.other) w = eld4(reinterpret_cast<const T*>(cs.other) + e);
+            o.x = chain_apply(cs.op, stored<T>(o.x), w.x, cs.scale);
+            o.y = chain_apply(cs.op, stored<T>(o.y), w.y, cs.scale);
+            o.z = chain_apply(cs.op, stored<T>(o.z), w.z, cs.scale);
+            o.w = chain_apply(cs.op, stored<T>(o.w), w.w, cs.scale);
+            est4(reinterpret_cast<T*>(cs.out) + e, o);
+          }
+        }
+      }
+      continue;
+    }
     if (d.vec == 4) {
       for (int64_t c = c0 + lane; c < c1; c += cstep) {
         float4 v[kMaxIn];
@@ -308,10 +349,11 @@ __global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __rest
 // source per descriptor, so a light kernel (few registers, full occupancy) with 8 independent
 // loads in flight per thread -- enough to cover NVLink latency on a peer read.
 template <class T>
-__global__ void __launch_bounds__(kThreads, 3) copy_kernel(const NaryDev* __restrict__ ds, int n, PeerSync sync) {
+__global__ void __launch_bounds__(kThreads, 3) copy_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
+                                                           PeerSync sync) {
   __shared__ int sdi;
   if (threadIdx.x == 0) {
-    const int di = find_desc(&ds[0].d.tile_begin, sizeof(NaryDev), n, blockIdx.x);
+    const int di = __ldg(tile_desc + blockIdx.x);
     sdi = di;
     if (ds[di].d.wait_mask) peer_wait(sync, ds[di].d.wait_mask, *sync.local);
   }
@@ -794,27 +836,27 @@ void nary_prepare(NaryBatch& b) {
   b.tiles = tiles;
   b.copy_only = true;
   for (const auto& d : b.descs) b.copy_only = b.copy_only && d.op == NARY_COPY && d.n_chain == 0;
+  std::vector<int> owner(static_cast<size_t>(tiles));
+  for (size_t i = 0; i < b.descs.size(); ++i) {
+    const int64_t end = i + 1 < b.descs.size() ? b.descs[i + 1].tile_begin : tiles;
+    for (int64_t q = b.descs[i].tile_begin; q < end; ++q) owner[size_t(q)] = int(i);
+  }
   upload(dev, &b.d_descs);
+  upload(owner, &b.d_tile_desc);
 }
 
 void nary_run(const NaryBatch& b, cudaStream_t s) {
   if (!b.tiles) return;
+  const NaryDev* ds = static_cast<const NaryDev*>(b.d_descs);
+  const int* td = static_cast<const int*>(b.d_tile_desc);
   if (b.copy_only) {
-    if (b.bf16)
-      copy_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
-                                                                        int(b.descs.size()), b.sync);
-    else
-      copy_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
-                                                                int(b.descs.size()), b.sync);
+    if (b.bf16) copy_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
+    else copy_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
     CUDA_CHECK(cudaGetLastError());
     return;
   }
-  if (b.bf16)
-    nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
-                                                                      int(b.descs.size()), b.sync);
-  else
-    nary_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(static_cast<const NaryDev*>(b.d_descs),
-                                                              int(b.descs.size()), b.sync);
+  if (b.bf16) nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
+  else nary_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -849,7 +891,9 @@ bool nary_add_chain(NaryDesc& d, const StridedView& d_out, int op, float scale, 
 
 void nary_free(NaryBatch& b) {
   if (b.d_descs) cudaFree(b.d_descs);
+  if (b.d_tile_desc) cudaFree(b.d_tile_desc);
   b.d_descs = nullptr;
+  b.d_tile_desc = nullptr;
 }
 
 uint64_t fnv1a(const char* s, size_t n) {

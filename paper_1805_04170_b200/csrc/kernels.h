@@ -91,6 +91,7 @@ struct NaryBatch {
   bool bf16 = false;  // storage type of every operand (arithmetic is fp32)
   bool pull = false;  // some descriptor reads peer memory (waits on PeerSync first)
   bool copy_only = false;  // every descriptor a plain copy: the light copy kernel (nary_prepare)
+  void* d_tile_desc = nullptr;  // int32 per block: its descriptor (no per-block search)
   PeerSync sync;
   std::vector<NaryDesc> descs;
   void* d_descs = nullptr;
