@@ -644,6 +644,11 @@ def main():
     suffix = "_bf16" if args.precision == "bf16" else ""
     for mode in ("opt", "data"):
         res[mode] = measure(mode, suffix, prec)
+    # N > 1: the optimal tiling of the TRAINING LOOP is the loop-consistent kcuts optimum (SURVEY
+    # finding 9 / §7 H1 (a): w and w_next tiled alike, every byte priced); the planner's
+    # single-step optimum (+ its unpriced w_next -> w carry) is reported beside it
+    if k >= 1 and all(plan_exists(p + suffix, "loop", k) for p in parts):
+        res["loop"] = measure("loop", suffix, prec)
     variants = {}
     if not args.no_variants:
         vsteps = max(5, min(args.steps, 20))
@@ -707,7 +712,9 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
-    o, d = res["opt"], res["data"]
+    d = res["data"]
+    o = res.get("loop", res["opt"])
+    single = res["opt"]
     flops = o["stats"]["gemm_flops"]
     tf32_peak = bf16_peak / 2
     peak = bf16_peak if args.precision == "bf16" else tf32_peak if prec == 0 else tf32_peak / 3
@@ -720,12 +727,18 @@ def main():
         "vs_baseline": None, "dtype": {"tf32": "tf32", "fp32": "fp32(3xtf32)", "bf16": "bf16"}[args.precision],
         "data": "synthetic",
         "config": dict(workload_config(args.config, k),
+                       plan=(f"loop-consistent kcuts optimum k={k} (unrolled-2-step planning through the unchanged "
+                             f"planner API, SURVEY finding 9)" if "loop" in res else f"kcuts optimal k={k}"),
                        exchange=("peer pull over NVLink (CUDA IPC), device-side phase counters" if peer else
                                  "NCCL send/recv per phase" if world > 1 else "one rank: HBM copies")),
         "dp": {"value": d["value"], "ms_per_step": d["ms_per_step"], "plan": f"preset data k={k}",
                "e2e": d["e2e"]["value"], "fetch_bytes_total": d["stats"]["fetch_bytes_total"],
                "carry_bytes_per_step": d["stats"]["carry_bytes"]},
         "opt_vs_dp": o["value"] / d["value"],
+        "opt_single_step": ({"value": single["value"], "ms_per_step": single["ms_per_step"],
+                             "plan": f"kcuts single-step optimum k={k} + its w_next -> w carry (unpriced by the planner)",
+                             "carry_bytes_per_step": single["stats"]["carry_bytes"],
+                             "vs_dp": single["value"] / d["value"]} if "loop" in res else None),
         "fetch_bytes_total": o["stats"]["fetch_bytes_total"],
         "carry_bytes_per_step": o["stats"]["carry_bytes"],
         "loop_carry": (f"{o['stats']['swapped']} weights carried by buffer swap (zero copy), "

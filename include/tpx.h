@@ -142,6 +142,11 @@ int tpx_execute_op(tpx_plan* plan, const char* op_id);
 /* Loop carry: after a train step, copy each `<w>_next` tensor's holder blocks onto `<w>`'s
  * holder blocks (conversion between their tilings, fetching across devices as needed). */
 int tpx_carry_weights(tpx_plan* plan);
+/* NumericCheck on the device (execute_numeric's comparison, simulator.cpp:129-147): every holder
+ * block of `tiled` on this rank against the same region of the one-device plan `serial`'s holder
+ * (both executed, same GPU and storage type); max |d|, max |d| / max(|truth|, 1), values compared.
+ * One reduction launch; nothing but the two maxima leaves the device. */
+int tpx_numeric_check(tpx_plan* tiled, tpx_plan* serial, double* max_abs, double* max_rel, int64_t* values);
 /* Waits for the plan stream; fails if a peer wait timed out (TPX_PEER_TIMEOUT_S, default 60 s). */
 int tpx_synchronize(tpx_plan* plan);
 

@@ -220,6 +220,14 @@ TPX_API int tpx_synchronize(tpx_plan* plan) {
   });
 }
 
+TPX_API int tpx_numeric_check(tpx_plan* tiled, tpx_plan* serial, double* max_abs, double* max_rel,
+                              int64_t* values) {
+  return tpx::guard([&] {
+    if (!max_abs || !max_rel || !values) tpx::fail("null output");
+    tpx::numeric_check(rt(tiled), rt(serial), max_abs, max_rel, values);
+  });
+}
+
 TPX_API int tpx_plan_ipc_handle(tpx_plan* plan, void* out, size_t len) {
   return tpx::guard([&] {
     if (!out) tpx::fail("null output buffer");

@@ -407,6 +407,47 @@ __global__ void __launch_bounds__(kThreads, 3) copy_kernel(const NaryDev* __rest
   }
 }
 
+// K7: max |got - want| and max |got - want| / max(|want|, 1) over a batch of (got, want) box
+// pairs, warp-reduced, one atomicMax per warp on the fp32 bit patterns (non-negative floats
+// order like their bits).
+template <class T>
+__global__ void __launch_bounds__(kThreads) check_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
+                                                         unsigned* __restrict__ out) {
+  const NaryDev& D = ds[__ldg(tile_desc + blockIdx.x)];
+  const NaryDesc& d = D.d;
+  const int64_t local = int64_t(blockIdx.x) - d.tile_begin;
+  const int64_t rb = local / D.n_col_chunks, cc = local % D.n_col_chunks;
+  const int64_t r0 = rb * D.rpt, r1 = min(D.rows, r0 + D.rpt);
+  const int64_t c0 = cc * D.col_chunk, c1 = min(D.inner, c0 + D.col_chunk);
+  const int rg = int(D.rg);
+  const int grp = int(threadIdx.x) / rg, lane = int(threadIdx.x) % rg;
+  float mabs = 0.f, mrel = 0.f;
+  for (int64_t r = r0 + grp; r < r1; r += kThreads / rg) {
+    const int64_t i2 = r % d.shape[2];
+    const int64_t t = r / d.shape[2];
+    const int64_t i1 = t % d.shape[1];
+    const int64_t i0 = t / d.shape[1];
+    const T* a = reinterpret_cast<const T*>(d.in[0]) + i0 * d.in_st[0][0] + i1 * d.in_st[0][1] + i2 * d.in_st[0][2];
+    const T* b = reinterpret_cast<const T*>(d.in[1]) + i0 * d.in_st[1][0] + i1 * d.in_st[1][1] + i2 * d.in_st[1][2];
+    for (int64_t c = c0 + lane; c < c1; c += rg) {
+      const float x = eld(a + c * d.in_st[0][3]), y = eld(b + c * d.in_st[1][3]);
+      const float diff = fabsf(x - y);
+      mabs = fmaxf(mabs, diff);
+      mrel = fmaxf(mrel, diff / fmaxf(fabsf(y), 1.f));
+      if (diff != diff) mabs = mrel = __int_as_float(0x7f800000);  // NaN: report infinity
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mabs = fmaxf(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+    mrel = fmaxf(mrel, __shfl_xor_sync(0xffffffffu, mrel, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, __float_as_uint(mabs));
+    atomicMax(out + 1, __float_as_uint(mrel));
+  }
+}
+
 // ---------------------------------------------------------------- init (seeded_tensor)
 
 struct InitDev {
@@ -857,6 +898,15 @@ void nary_run(const NaryBatch& b, cudaStream_t s) {
   }
   if (b.bf16) nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
   else nary_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void numeric_check_run(const NaryBatch& b, unsigned* dev_out, cudaStream_t s) {
+  if (!b.tiles) return;
+  const NaryDev* ds = static_cast<const NaryDev*>(b.d_descs);
+  const int* td = static_cast<const int*>(b.d_tile_desc);
+  if (b.bf16) check_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, dev_out);
+  else check_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, dev_out);
   CUDA_CHECK(cudaGetLastError());
 }
 

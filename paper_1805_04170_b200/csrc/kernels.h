@@ -108,6 +108,11 @@ NaryDesc nary_desc(int op, const StridedView& out, const std::vector<StridedView
 bool nary_add_chain(NaryDesc& d, const StridedView& d_out, int op, float scale, const StridedView& out,
                     const StridedView* other, int esize);
 void nary_prepare(NaryBatch& b);  // uploads descriptor table
+// K7, the on-device NumericCheck reduction (simulator.cpp:129-147): over every descriptor of b
+// (in[0] = the tiled value, in[1] = the single-device truth over the same region), the max of
+// |d| and of |d| / max(|truth|, 1) into dev_out[0..1] (fp32 bit patterns, atomically max-ed;
+// both are >= 0).  b must be prepared.
+void numeric_check_run(const NaryBatch& b, unsigned* dev_out, cudaStream_t s);
 void nary_run(const NaryBatch& b, cudaStream_t s);
 void nary_free(NaryBatch& b);
 

@@ -1616,6 +1616,63 @@ static const StridedView& node_val(PlanRt& P, int node, int64_t n) {
   return v;
 }
 
+// NumericCheck on the device (simulator.cpp:129-147): every holder block of the
+// tiled plan on this rank against the same region of the single-device plan's holder, max |d|
+// and max |d| / max(|truth|, 1) reduced by one launch; only two floats come back.
+void numeric_check(PlanRt& T, PlanRt& S, double* max_abs, double* max_rel, int64_t* values) {
+  if (T.esize != S.esize) fail("numeric check: the plans store different element types");
+  if (S.plan.devices != 1) fail("numeric check: the truth must be a one-device plan");
+  g_es = T.esize;
+  CUDA_CHECK(cudaStreamSynchronize(S.stream));
+  CUDA_CHECK(cudaStreamSynchronize(T.stream));
+  NaryBatch b;
+  b.bf16 = T.esize == 2;
+  int64_t n = 0;
+  for (const auto& kv : T.plan.holders) {
+    auto it = S.plan.holders.find(kv.first);
+    if (it == S.plan.holders.end() || it->second.empty()) fail("numeric check: tensor " + kv.first + " has no truth");
+    const int sn = it->second[0];
+    const PlanNode& snode = S.plan.nodes[size_t(sn)];
+    const StridedView& sv = node_val(S, sn, snode.region.volume());
+    for (int h : kv.second) {
+      if (h < 0 || !T.mine(h)) continue;
+      const PlanNode& hn = T.plan.nodes[size_t(h)];
+      if (hn.region.volume() == 0) continue;
+      const StridedView& tv = node_val(T, h, hn.region.volume());
+      const StridedView want = subview(sv, snode.region, hn.region);
+      NaryDesc d = nary_desc(NARY_COPY, want, {tv, want}, 0.f, T.esize);
+      d.vec = 1;
+      d.units = tv.elements();
+      b.descs.push_back(d);
+      n += tv.elements();
+    }
+  }
+  *max_abs = *max_rel = 0;
+  *values = n;
+  if (b.descs.empty()) return;
+  nary_prepare(b);
+  unsigned* dev = nullptr;
+  unsigned host[2] = {0, 0};
+  try {
+    CUDA_CHECK(cudaMalloc(&dev, 2 * sizeof(unsigned)));
+    CUDA_CHECK(cudaMemsetAsync(dev, 0, 2 * sizeof(unsigned), T.stream));
+    numeric_check_run(b, dev, T.stream);
+    CUDA_CHECK(cudaMemcpyAsync(host, dev, sizeof host, cudaMemcpyDeviceToHost, T.stream));
+    CUDA_CHECK(cudaStreamSynchronize(T.stream));
+  } catch (...) {
+    if (dev) cudaFree(dev);
+    nary_free(b);
+    throw;
+  }
+  cudaFree(dev);
+  nary_free(b);
+  float fa, fr;
+  std::memcpy(&fa, &host[0], 4);
+  std::memcpy(&fr, &host[1], 4);
+  *max_abs = fa;
+  *max_rel = fr;
+}
+
 // Raw storage-type I/O: n elements of the plan's storage type (fp32 or bf16) in host memory.
 void read_node_f32(PlanRt& P, int node, float* dst, int64_t n) {
   g_es = P.esize;

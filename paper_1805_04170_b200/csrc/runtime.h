@@ -160,5 +160,7 @@ void write_node(PlanRt& p, int node, const double* src, int64_t n);
 void read_node_f32(PlanRt& p, int node, float* dst, int64_t n);
 void write_node_f32(PlanRt& p, int node, const float* src, int64_t n);
 std::string describe(const PlanRt& p);
+// K7: NumericCheck of plan t's holders on this rank against the one-device plan s (same GPU).
+void numeric_check(PlanRt& t, PlanRt& s, double* max_abs, double* max_rel, int64_t* values);
 
 }  // namespace tpx

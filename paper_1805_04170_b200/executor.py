@@ -263,6 +263,37 @@ def serial_plan(graph: dict) -> str:
                        "fetch_bytes_total": 0})
 
 
+def execute_numeric_host(plan_json: str, seed: int, ctx: Optional[Context] = None,
+                         precision: int = PREC_TF32, flags: int = FLAG_FUSE) -> NumericCheck:
+    """The same check with the comparison on the host (every holder read back): cross-checks the
+    device reduction in the tests."""
+    ctx = ctx or Context(0)
+    plan = json.loads(plan_json)
+    tiled = PlanExecutor(ctx, plan_json, precision, flags)
+    serial = PlanExecutor(ctx, serial_plan(plan["graph"]), precision, flags)
+    for ex in (tiled, serial):
+        ex.init_inputs(seed)
+        ex.execute()
+        ex.synchronize()
+    c = NumericCheck(seed=seed)
+    nodes = {n["id"]: n for n in plan["nodes"]}
+    for tid, hs in plan["holders"].items():
+        full = serial.read_node(serial.holders()[tid][0])
+        for d, hid in enumerate(hs):
+            if d not in tiled.my_devices():
+                continue
+            reg = nodes[hid]["region"]
+            want = full[tuple(slice(lo, hi) for lo, hi in reg)]
+            diff = np.abs(tiled.read_node(hid) - want)
+            if diff.size:
+                c.max_abs = max(c.max_abs, float(diff.max()))
+                c.max_rel = max(c.max_rel, float((diff / np.maximum(np.abs(want), 1.0)).max()))
+            c.values += diff.size
+    tiled.close()
+    serial.close()
+    return c
+
+
 def execute_numeric(plan_json: str, seed: int, ctx: Optional[Context] = None,
                     precision: int = PREC_TF32, flags: int = FLAG_FUSE) -> NumericCheck:
     """B200 counterpart of execute_numeric (simulator.cpp:55-149): the tiled plan and the
@@ -282,23 +313,11 @@ def execute_numeric(plan_json: str, seed: int, ctx: Optional[Context] = None,
     serial.execute()
     tiled.synchronize()
     serial.synchronize()
-    c = NumericCheck(seed=seed)
-    nodes = {n["id"]: n for n in plan["nodes"]}
-    for tid, hs in plan["holders"].items():
-        full = serial.read_node(serial.holders()[tid][0])
-        for d, hid in enumerate(hs):
-            if not hid:
-                raise TpxError(f"tensor {tid} has no holder on some device")
-            if d not in tiled.my_devices():
-                continue
-            reg = nodes[hid]["region"]
-            want = full[tuple(slice(lo, hi) for lo, hi in reg)]
-            got = tiled.read_node(hid)
-            diff = np.abs(got - want)
-            if diff.size:
-                c.max_abs = max(c.max_abs, float(diff.max()))
-                c.max_rel = max(c.max_rel, float((diff / np.maximum(np.abs(want), 1.0)).max()))
-            c.values += diff.size
+    # the comparison runs on the device (tpx_numeric_check): one reduction over
+    # every holder block of this rank; only max |d|, max rel and the count come back
+    ma, mr, nv = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+    check(lib().tpx_numeric_check(tiled._h, serial._h, ctypes.byref(ma), ctypes.byref(mr), ctypes.byref(nv)))
+    c = NumericCheck(max_abs=ma.value, max_rel=mr.value, values=nv.value, seed=seed)
     tiled.close()
     serial.close()
     return c

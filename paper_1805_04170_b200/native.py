@@ -46,6 +46,7 @@ _SIGS = {
     "tpx_load_plan": [c_vp, c_char_p, ctypes.c_size_t, c_int, c_int, P(c_vp)],
     "tpx_plan_free": [c_vp],
     "tpx_plan_ipc_handle": [c_vp, c_vp, ctypes.c_size_t],
+    "tpx_numeric_check": [c_vp, c_vp, P(c_dbl), P(c_dbl), P(c_i64)],
     "tpx_plan_connect_peers": [c_vp, c_vp, ctypes.c_size_t],
     "tpx_plan_stats": [c_vp, P(Stats)],
     "tpx_plan_describe": [c_vp, P(c_vp)],

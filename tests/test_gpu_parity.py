@@ -233,6 +233,20 @@ def test_execute_numeric_mirror(ctx):
     assert c.max_rel <= 1e-5
 
 
+@pytest.mark.parametrize("stem", [s for s in STEMS if any(x in s for x in (
+    "mlp_train_d4.opt.k2.s17", "cfg1_bf16.opt.k1", "alexr_conv_b4.opt.k1", "fcr_alexnet_b32.opt.k3"))], ids=stem_id)
+def test_numeric_check_on_device_matches_host(ctx, stem):
+    """K7: tpx_numeric_check's one-launch reduction gives exactly the host comparison's maxima
+    (fp32 subtraction and division in both; the host reads the same stored values)."""
+    from paper_1805_04170_b200.executor import PREC_TF32, execute_numeric, execute_numeric_host
+    text, P, seed, _, _ = oracle_values(stem)
+    dev = execute_numeric(text, seed, ctx, precision=PREC_TF32)
+    host = execute_numeric_host(text, seed, ctx, precision=PREC_TF32)
+    assert dev.values == host.values > 0
+    assert dev.max_abs == pytest.approx(host.max_abs, rel=1e-6, abs=1e-12)
+    assert dev.max_rel == pytest.approx(host.max_rel, rel=1e-6, abs=1e-12)
+
+
 def test_bad_plan_fails_loudly(ctx):
     from paper_1805_04170_b200.executor import PlanExecutor, TpxError
     stem = [s for s in STEMS if "mlp_train_d1.opt.k1" in s][0]
