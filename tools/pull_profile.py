@@ -26,6 +26,10 @@ ex.execute()
 times = ex.last_step_times()
 steps = ex.describe()["main"]["steps"]
 rows = []
+syncs = [t for t, s in zip(times, steps) if s["kind"] == "sync"]
+if syncs:
+    print(f"sync steps: {len(syncs)}, {sum(syncs) * 1e3:.1f} us total, {sum(syncs) / len(syncs) * 1e3:.2f} us each "
+          f"(step total {sum(times) * 1e3:.1f} us)")
 for t, s in zip(times, steps):
     if s["kind"] == "nary":
         gbs = s["bytes"] / (t * 1e-3) / 1e9 if t > 0 else 0
