@@ -708,6 +708,7 @@ def main():
             cpu = {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    xin = max_over_ranks(float(res.get("loop", res["opt"])["stats"]["rank_xrank_bytes_in"]))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -716,6 +717,9 @@ def main():
     o = res.get("loop", res["opt"])
     single = res["opt"]
     flops = o["stats"]["gemm_flops"]
+    # north_star step roofline per GPU: max(FLOPs at the tensor peak, received bytes at NVLink
+    # bandwidth); the HBM term of the GEMMs is reported beside it
+    nvl_bw = 900e9  # NVLink 5 per direction per GPU (B200 datasheet; not measurable on one GPU)
     tf32_peak = bf16_peak / 2
     peak = bf16_peak if args.precision == "bf16" else tf32_peak if prec == 0 else tf32_peak / 3
     kernels, dom = kernel_rooflines(o, peak, hbm_peak)
@@ -761,7 +765,19 @@ def main():
                      "timing_pass": ("per-launch CUDA events between every lowered step, graph replay off; "
                                      "shares are of that pass's total"),
                      "step_roofline_ms": step_roofline_ms(kernels),
-                     "step_frac": step_roofline_ms(kernels) / o["ms_per_step"]},
+                     "step_frac": step_roofline_ms(kernels) / o["ms_per_step"],
+                     "north_star_step": {
+                         "tensor_ms": flops / (peak * 1e12) * 1e3,
+                         "nvlink_ms": xin / nvl_bw * 1e3,
+                         "hbm_gemm_ms": step_roofline_ms(kernels),
+                         "roofline_ms": max(flops / (peak * 1e12) * 1e3, xin / nvl_bw * 1e3),
+                         "frac": max(flops / (peak * 1e12) * 1e3, xin / nvl_bw * 1e3) / o["ms_per_step"],
+                         "frac_3term": max(flops / (peak * 1e12) * 1e3, xin / nvl_bw * 1e3,
+                                           step_roofline_ms(kernels)) / o["ms_per_step"],
+                         "received_bytes_per_gpu": xin,
+                         "basis": "per GPU: this rank's GEMM FLOPs at the measured tensor peak; the most bytes any "
+                                  "rank pulls from other ranks at 900 GB/s NVLink; hbm_gemm_ms = sum over GEMM "
+                                  "launches of max(FLOPs/tensor peak, bytes/HBM peak)"}},
         "clocks": o["clocks"],
         "cpu_baseline": cpu,
         "variants": variants,

@@ -102,6 +102,10 @@ typedef struct tpx_plan tpx_plan;
  * the plan runs only after tpx_plan_connect_peers; with world = 1 and TPX_FLAG_FORCE_XCHG every
  * cross-device fetch takes this path against the rank's own arena. */
 #define TPX_FLAG_PEER 32
+/* Conv grad_input GEMMs on K-major transposed copies of the filter and the gradient instead of
+ * the stored MN-major operands (kind::tf32 reads MN-major operands at about half rate; the
+ * transposes cost about what the faster GEMM saves, so this is opt-in). */
+#define TPX_FLAG_KMAJOR_CONV 64
 int tpx_load_plan(tpx_ctx* ctx, const char* plan_json, size_t len, int precision, int flags,
                   tpx_plan** out);
 /* TPX_FLAG_PEER, world > 1: this rank's arena as a CUDA IPC handle (64 bytes) ... */

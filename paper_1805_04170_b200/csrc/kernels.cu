@@ -757,12 +757,48 @@ __device__ __forceinline__ void shiftpad_body(const ConvDesc& d, int tile) {
   }
 }
 
+// 64 x 64 tiles of a 2-D transpose through shared memory (padded rows: conflict-free both
+// ways), kTrTiles consecutive column tiles per block; every thread keeps its 16 loads in flight
+// before the shared-memory writes.  Reads and writes are 256-byte coalesced runs.
+constexpr int kTrTiles = 4;
+template <class T>
+__device__ __forceinline__ void transpose_body(const ConvDesc& d, int tile) {
+  extern __shared__ __align__(16) unsigned char move_smem[];
+  T* sm = reinterpret_cast<T*>(move_smem);  // [64][65]
+  const int64_t R = d.a.shape[0], C = d.a.shape[1], rs = d.a.st[0], ot = d.p[0];
+  const int64_t tcg = (C + 64 * kTrTiles - 1) / (64 * kTrTiles);
+  const int64_t r0 = (tile / tcg) * 64, cg0 = (tile % tcg) * 64 * kTrTiles;
+  const T* src = reinterpret_cast<const T*>(d.a.ptr);
+  T* dst = reinterpret_cast<T*>(d.out);
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4 threads
+  for (int t = 0; t < kTrTiles; ++t) {
+    const int64_t c0 = cg0 + 64 * t;
+    if (c0 >= C) break;
+    T v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int64_t r = r0 + ty + 4 * j, c = c0 + tx;
+      if (r < R && c < C) v[j] = src[r * rs + c];
+    }
+    if (t > 0) __syncthreads();  // the previous tile's reads of sm are done
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sm[(ty + 4 * j) * 65 + tx] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int64_t c = c0 + ty + 4 * j, r = r0 + tx;
+      if (c < C && r < R) dst[c * ot + r] = sm[tx * 65 + ty + 4 * j];
+    }
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(kThreads) premove_kernel(const ConvDesc* __restrict__ ds, int n) {
   const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
   const ConvDesc& d = ds[di];
   const int tile = int(int64_t(blockIdx.x) - d.tile_begin);
   if (d.mode == CONV_IM2COL) im2col_body<T>(d, tile);
+  else if (d.mode == CONV_TRANSPOSE) transpose_body<T>(d, tile);
   else shiftpad_body<T>(d, tile);
 }
 
@@ -993,15 +1029,31 @@ void conv_prepare(ConvBatch& b) {
   int64_t tiles = 0;
   b.move = !b.descs.empty() && b.descs[0].mode >= CONV_IM2COL;
   b.smem = 0;
+  b.bytes = 0;
   const int64_t es = b.bf16 ? 2 : 4;
   for (auto& d : b.descs) {
+    if (d.mode == CONV_IM2COL) {  // input read once, every column written
+      b.bytes += double(es) * (double(d.a.elements()) +
+                               double(d.a.shape[1] * d.p[0] * d.p[1]) * double(d.a.shape[0] * d.p[2] * d.p[3]));
+    } else if (d.mode == CONV_COL2IM) {  // every column read once, h (and 1 - tanh^2 h) written
+      const double outs = double(d.n) * double(d.p[4] + d.p[2] - 1);
+      b.bytes += double(es) * (double(d.p[0] * d.p[1] * d.p[2]) * double(d.a.shape[0] * d.p[3] * d.p[4]) +
+                               outs * (d.b.ptr ? 2.0 : 1.0));
+    } else if (d.mode == CONV_SHIFTPAD) {
+      b.bytes += double(es) * double(d.a.elements()) * double(1 + d.p[0]);
+    } else if (d.mode == CONV_TRANSPOSE) {
+      b.bytes += 2.0 * double(es) * double(d.a.shape[0] * d.a.shape[1]);
+    }
     if ((d.mode >= CONV_IM2COL) != b.move) throw std::runtime_error("conv batch mixes compute and data movement");
     if (b.move && (d.mode == CONV_COL2IM) != (b.descs[0].mode == CONV_COL2IM))
       throw std::runtime_error("conv batch mixes col2im with pre-GEMM movement");
     d.tile_begin = tiles;
     if (b.move) {
       const int64_t NB = std::max<int64_t>(d.a.shape[0], 1);
-      if (d.mode == CONV_SHIFTPAD) {
+      if (d.mode == CONV_TRANSPOSE) {
+        tiles += ((d.a.shape[0] + 63) / 64) * ((d.a.shape[1] + 64 * kTrTiles - 1) / (64 * kTrTiles));
+        b.smem = std::max<int64_t>(b.smem, 64 * 65 * es);
+      } else if (d.mode == CONV_SHIFTPAD) {
         const int64_t YX = std::max<int64_t>(d.p[1] * d.p[2], 1);
         const int64_t G = std::min(NB, std::max<int64_t>(1, (4 * kThreads + YX - 1) / YX));
         d.p[7] = G;

@@ -150,6 +150,10 @@ enum ConvModeCode : int {
                          //   (p = V,Yo,Xo,Wp,Sp,vstride,ld): a [n,o,y,x] view copied into a
                          //   channel-major grid, V column-shifted copies (V = 1: the gradient
                          //   permuted for grad_weight)
+  CONV_TRANSPOSE = 7,    // out[c * p0 + r] = a[r * a.st[0] + c] for r < a.shape[0], c < a.shape[1]
+                         //   (a rank-2 row-major view; p0 = the transposed rows' pitch): operands
+                         //   made K-major for the tensor cores (kind::tf32 reads MN-major operands
+                         //   at about half rate)
   CONV_COL2IM = 5,       // out[n,c,y,x] = sum_{u,v} col[(c*U*V+u*V+v)*pitch + n*img + (y-u)*Xo+(x-v)]
                          //   (a.ptr = col, a.shape[0] = N, p = C,U,V,Yo,Xo,pitch,img; taps in
                          //   ascending (u, v) order; b.ptr != null: also b[...] = 1 - tanh(out)^2;
@@ -173,6 +177,7 @@ struct ConvBatch {
   bool move = false;  // im2col / col2im batch (d.n counts rows) rather than direct conv
   int64_t smem = 0;   // dynamic shared memory of the im2col launch
   bool bf16 = false;  // storage type
+  double bytes = 0;   // algorithmic bytes of a data-movement batch (im2col / col2im / copies)
 };
 void conv_prepare(ConvBatch& b);
 void conv_run(const ConvBatch& b, cudaStream_t s);

@@ -131,8 +131,13 @@ struct Lowerer {
 
   Lowerer(PlanRt& p, Program& pr, bool d)
       : P(p), pl(p.plan), C(*p.ctx), prog(pr), dry(d),
-        fuse(p.flags & 1), force_xchg(p.flags & 2), tc_conv(!(p.flags & 4)) {}
+        fuse(p.flags & 1), force_xchg(p.flags & 2), tc_conv(!(p.flags & 4)),
+        transposed_operands((p.flags & 64) != 0) {}
   bool tc_conv;
+  // conv grad_input on K-major transposed operands (TPX_FLAG_KMAJOR_CONV = 64, opt-in: measured
+  // +/- 1 % on the AlexNet-style step, -2.5 % on the VGG-style one: the transposes cost what the
+  // faster GEMM saves)
+  bool transposed_operands;
   std::map<std::vector<int64_t>, float*> col_cache;  // im2col buffers by (view, filter) key
   std::map<std::vector<int64_t>, float*> gp_cache;   // permuted conv gradients by (view, pitch)
 
@@ -535,12 +540,25 @@ struct Lowerer {
       const MatView km = filter(b);
       const int64_t img = pitch4(YX), ld = pitch4(NB * img);
       // the padding columns of Gp are 0, so dcol's are too (col2im never reads them)
+      const size_t npre = o_prec.descs.size();
       float* gp = permuted_grad(a, img, ld, op.id);
+      // (a Gp permuted in this very launch cannot be transposed by it: stored operands then)
+      const bool gp_fresh = o_prec.descs.size() != npre;
       float* dcol = alloc_bytes(size_t(K * ld) * size_t(g_es));
       GemmSpec s;
-      s.a = km;  // Kmat [o, cuv], used transposed
-      s.ta = true;
-      s.b = MatView{gp, O, NB * img, ld, 1};
+      if (transposed_operands && !gp_fresh) {
+        // both operands K-major (contraction over o contiguous): Kmatᵀ [cuv][o] and Gpᵀ [(n,yx)][o],
+        // made by the pre-GEMM transposes (kind::tf32 reads MN-major operands at about half
+        // rate; the transposes cost 2 x (filter + gradient) bytes)
+        const int64_t op4 = pitch4(O);
+        s.a = MatView{transposed(km.ptr, km.rows, km.cols, km.rs, op4, op.id), K, O, op4, 1};
+        s.b = MatView{transposed(gp, O, NB * img, ld, op4, op.id), NB * img, O, op4, 1};
+        s.tb = true;
+      } else {
+        s.a = km;  // Kmat [o, cuv], used transposed
+        s.ta = true;
+        s.b = MatView{gp, O, NB * img, ld, 1};
+      }
       s.c = dcol;
       s.c_rs = ld;
       specs.push_back(s);
@@ -587,6 +605,33 @@ struct Lowerer {
     d.p[0] = 1; d.p[1] = Yo; d.p[2] = Xo; d.p[3] = Xo; d.p[4] = img; d.p[5] = 0; d.p[6] = ld;
     o_prec.descs.push_back(d);
     return gp;
+  }
+
+  // dst[c][r] = src[r][c] (rows x cols, source row stride rs) into fresh storage with `pitch`
+  // elements per transposed row (pre class: runs before the op's GEMM), cached per source.
+  std::map<std::vector<int64_t>, float*> tr_cache;
+  float* transposed(const float* src, int64_t rows, int64_t cols, int64_t rs, int64_t pitch, const std::string& op) {
+    const std::vector<int64_t> key = {int64_t(reinterpret_cast<uintptr_t>(src)), rows, cols, rs, pitch};
+    auto hit = tr_cache.find(key);
+    if (hit != tr_cache.end()) return hit->second;
+    if (!o_prec.descs.empty() && o_pre_op != op) flush();
+    o_pre_op = op;
+    float* dst = alloc_bytes(size_t(cols * pitch) * size_t(g_es));
+    ConvDesc d;
+    std::memset(&d, 0, sizeof d);
+    d.mode = CONV_TRANSPOSE;
+    d.a.ptr = const_cast<float*>(src);
+    d.a.rank = 2;
+    d.a.shape[0] = rows;
+    d.a.shape[1] = cols;
+    d.a.st[0] = rs;
+    d.a.st[1] = 1;
+    d.out = dst;
+    d.p[0] = pitch;
+    d.n = rows * cols;
+    o_prec.descs.push_back(d);
+    tr_cache[key] = dst;
+    return dst;
   }
 
   StridedView materialize(int node, const std::string& op) {
@@ -1810,7 +1855,8 @@ std::string describe(const PlanRt& P) {
         }
         s << "],\"bytes_in\":" << g.bytes_in << ",\"bytes_out\":" << g.bytes_out;
       } else if (st.kind == ST_CONV) {
-        s << ",\"descs\":" << prog.conv[size_t(st.idx)].descs.size();
+        s << ",\"descs\":" << prog.conv[size_t(st.idx)].descs.size()
+          << ",\"bytes\":" << int64_t(prog.conv[size_t(st.idx)].bytes);
       } else if (st.kind == ST_SYNC) {
         s << ",\"barrier\":" << st.barrier;
       }

@@ -129,6 +129,13 @@ def test_per_op_tf32(ctx, stem):
     assert e <= (TOL_OP_BF16 if is_bf16(stem) else TOL_OP[0]), (op, e)
 
 
+@pytest.mark.parametrize("stem", [s for s in STEMS if "conv" in s or "cnn" in s][::3], ids=stem_id)
+def test_kmajor_conv_per_op(ctx, stem):
+    """TPX_FLAG_KMAJOR_CONV (conv grad_input on transposed K-major operands): same per-op gates."""
+    e, op = run_per_op(ctx, stem, 0 if is_bf16(stem) else 1, flags=64)
+    assert e <= (TOL_OP_BF16 if is_bf16(stem) else TOL_OP[1]), (op, e)
+
+
 @pytest.mark.parametrize("stem", STEMS, ids=stem_id)
 def test_chained_fp32(ctx, stem):
     if is_bf16(stem):

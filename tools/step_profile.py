@@ -13,7 +13,7 @@ from paper_1805_04170_b200.executor import FLAG_FUSE, Context, PlanExecutor  # n
 stem = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 text = gzip.open(os.path.join(ROOT, "plans", stem + ".plan.json.gz"), "rt").read()
-ex = PlanExecutor(Context(0), text, precision=0, flags=FLAG_FUSE)
+ex = PlanExecutor(Context(0), text, precision=0, flags=FLAG_FUSE | int(os.environ.get("TPX_EXTRA_FLAGS", "0")))
 ex.init_inputs(7)
 for _ in range(3):
     ex.execute()
@@ -33,5 +33,6 @@ for st, t in zip(steps, ms):
 for key, t in sorted(by.items(), key=lambda kv: -kv[1]):
     print(f"  {key[0]:5s} {key[1]:12s} {t:8.3f} ms {100 * t / tot:5.1f}%")
 for st, t in sorted(zip(steps, ms), key=lambda p: -p[1])[:top]:
-    extra = st.get("shapes", [[]])[0] if st["kind"] == "gemm" else st.get("descs", st.get("bytes", ""))
-    print(f"  {t:8.3f} ms  {st['kind']:5s} {st['what']:12s} {st['op']:10s} {extra}")
+    extra = st.get("shapes", [[]])[0] if st["kind"] == "gemm" else st.get("descs", "")
+    gbs = f"{st['bytes'] / (t * 1e-3) / 1e9:7.0f} GB/s" if st.get("bytes") and st["kind"] != "gemm" else ""
+    print(f"  {t:8.3f} ms  {st['kind']:5s} {st['what']:12s} {st['op']:10s} {extra} {gbs}")
