@@ -1222,6 +1222,8 @@ bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-i
 int g_odepth = 0;      // debug (15, n): operand ring depth n (0 = chosen from the smem budget)
 int g_min_stages = 4;  // debug (16, n): mainloop stages the operand ring must leave
 int g_ts_chain = 0;    // debug (18, n): TMA-store epilogue also for chains (n = 1 single, 2 double-buffered boxes)
+int g_rr_tiles = 1;    // debug (20, n): whole-tile schedules dealt round-robin (1, default) or in contiguous blocks (0)
+int g_tq_block = 0;    // debug (21, n): tile list in blocks of n Q-tiles (0 = Q-tile major)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1324,7 +1326,9 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 15) g_odepth = int(sbo);             // (15,n) epilogue operand ring depth n
   if (lbo == 16) g_min_stages = int(sbo);         // (16,n) keep >= n mainloop stages
   if (lbo == 18) g_ts_chain = int(sbo);           // (18,n) TMA-store chain epilogues
-  if (lbo >= 1 && lbo <= 18) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
+  if (lbo == 20) g_rr_tiles = int(sbo);           // (20,n) round-robin whole tiles
+  if (lbo == 21) g_tq_block = int(sbo);           // (21,n) Q-tile blocks in the tile list
+  if (lbo >= 1 && lbo <= 21) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1353,9 +1357,17 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
   std::vector<SchedCol> cols;
   for (int pi = 0; pi < int(probs.size()); ++pi) {
     const GemmProblem& pr = probs[size_t(pi)];
-    for (int tq = 0; tq < pr.tiles_q; ++tq)
+    // Q-tile major, or (debug) blocks of B Q-tiles walked P-tile major inside, so the tiles in
+    // flight share fewer operand panels
+    const int B = g_tq_block > 0 ? g_tq_block : pr.tiles_q;
+    for (int tb = 0; tb < pr.tiles_q; tb += B)
       for (int tp0 = 0; tp0 < pr.tiles_p; tp0 += G)
-        cols.push_back({pi, tq, tp0, std::min(G, pr.tiles_p - tp0), pr.kb_total});
+        for (int tq = tb; tq < std::min(pr.tiles_q, tb + B); ++tq)
+          if (g_tq_block > 0) cols.push_back({pi, tq, tp0, std::min(G, pr.tiles_p - tp0), pr.kb_total});
+    if (g_tq_block <= 0)
+      for (int tq = 0; tq < pr.tiles_q; ++tq)
+        for (int tp0 = 0; tp0 < pr.tiles_p; tp0 += G)
+          cols.push_back({pi, tq, tp0, std::min(G, pr.tiles_p - tp0), pr.kb_total});
   }
   long long U = 0;
   for (const auto& c : cols) U += c.kb;
@@ -1402,6 +1414,14 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
       std::stable_sort(gp.begin(), gp.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
         return (a.second > 0) > (b.second > 0);
       });
+  } else if (whole && g_rr_tiles) {
+    // tile c to group c mod groups: the groups walk the tile list side by side, so the tiles in
+    // flight at any moment are neighbours (one problem, shared operand panels in L2)
+    for (int c = 0; c < ncols; ++c) {
+      const int g = c % groups;
+      pieces[size_t(c)].push_back({g, 0, cols[size_t(c)].kb});
+      group_pieces[size_t(g)].push_back({c, 0});
+    }
   } else if (whole) {
     for (int g = 0; g < groups; ++g) {
       const int c0 = int((long long)ncols * g / groups), c1 = int((long long)ncols * (g + 1) / groups);

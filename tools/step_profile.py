@@ -10,6 +10,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1805_04170_b200.executor import FLAG_FUSE, Context, PlanExecutor  # noqa: E402
 
+for kv in filter(None, os.environ.get("TPX_GEMM_KNOBS", "").split(",")):  # gemm.cu debug knobs
+    import ctypes
+    from paper_1805_04170_b200 import native
+    k, v = kv.split(":")
+    native.lib().tpx_debug_gemm_mn_desc(ctypes.c_uint(int(k)), ctypes.c_uint(int(v)))
 stem = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 text = gzip.open(os.path.join(ROOT, "plans", stem + ".plan.json.gz"), "rt").read()
