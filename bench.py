@@ -375,7 +375,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1805_04170_b200.executor import (FLAG_FORCE_XCHG, FLAG_FUSE, FLAG_GRAPH, FLAG_LOOP, FLAG_PEER,
-                                                Context, PlanExecutor)
+                                                FLAG_PEER_SOLO, Context, PlanExecutor)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -496,6 +496,54 @@ def main():
         if tm:
             r["time_model"] = tm
         return r
+
+    def n_gpu_projection(steps):
+        """One rank's share of an N-GPU step, measured on this GPU (TPX_FLAG_PEER_SOLO: the rank's
+        own program -- its GEMMs on its shards, its pull launches reading local HBM instead of
+        NVLink, its sync points already satisfied), for ranks 0 and N-1 of N = 2, 4, 8.  The
+        projection adds the rank's pulled bytes at NVLink 5 bandwidth (900 GB/s per direction)
+        without overlap: projected step = max over the two ranks of (measured + bytes / 900 GB/s).
+        A projection from measured per-GPU work, not a multi-GPU measurement."""
+        out = {}
+        for kk in (1, 2, 3):
+            row = {}
+            for mode in ("loop", "opt", "data"):
+                if not all(plan_exists(p + suffix, mode, kk) for p in parts):
+                    continue
+                per_rank = []
+                for rk in sorted({0, (1 << kk) - 1}):
+                    sctx = Context(local, rk, 1 << kk)
+                    exs = []
+                    try:
+                        for part in parts:
+                            ex = PlanExecutor(sctx, load_plan(part + suffix, mode, kk), precision=prec,
+                                              flags=base_flags | FLAG_PEER | FLAG_PEER_SOLO)
+                            ex.set_stream(stream.cuda_stream)
+                            ex.init_inputs(SEED)
+                            exs.append(ex)
+
+                        def step():
+                            for ex in exs:
+                                ex.execute()
+                        for _ in range(args.warmup):
+                            step()
+                        ms = timed(step, stream, steps, barrier) / steps
+                        xin = sum(ex.stats()["rank_xrank_bytes_in"] for ex in exs)
+                    finally:
+                        for ex in exs:
+                            ex.close()
+                        sctx.close()
+                    per_rank.append({"rank": rk, "measured_ms": ms, "pulled_bytes": xin,
+                                     "projected_ms": ms + xin / 900e9 * 1e3})
+                proj = max(r["projected_ms"] for r in per_rank)
+                row[mode] = {"per_rank": per_rank, "projected_ms_per_step": proj,
+                             "projected_samples_per_s": batch / (proj / 1e3)}
+            if "data" in row:
+                for m in ("loop", "opt"):
+                    if m in row:
+                        row[f"{m}_vs_dp"] = row[m]["projected_samples_per_s"] / row["data"]["projected_samples_per_s"]
+            out[f"N{1 << kk}"] = row
+        return out
 
     def measure(mode, suffix, prec):
         """One plan set (every component of the workload) timed end to end."""
@@ -683,6 +731,7 @@ def main():
                             row[f"{lab}_vs_dp"] = row[lab]["value"] / row["data"]["value"]
                 tiled[f"k{kk}"] = row
             variants["tiled_one_gpu"] = tiled
+            variants["n_gpu_projection"] = n_gpu_projection(vsteps)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

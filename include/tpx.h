@@ -106,6 +106,11 @@ typedef struct tpx_plan tpx_plan;
  * the stored MN-major operands (kind::tf32 reads MN-major operands at about half rate; the
  * transposes cost about what the faster GEMM saves, so this is opt-in). */
 #define TPX_FLAG_KMAJOR_CONV 64
+/* With TPX_FLAG_PEER and world > 1: run this rank alone, every peer arena stood in for by the
+ * rank's own (no tpx_plan_connect_peers).  The rank's program is unchanged -- its compute, its
+ * pull launches reading local HBM instead of NVLink, its sync points (already satisfied) -- so
+ * one GPU measures one rank's share of an N-GPU step.  Values are meaningless; timing only. */
+#define TPX_FLAG_PEER_SOLO 128
 int tpx_load_plan(tpx_ctx* ctx, const char* plan_json, size_t len, int precision, int flags,
                   tpx_plan** out);
 /* TPX_FLAG_PEER, world > 1: this rank's arena as a CUDA IPC handle (64 bytes) ... */

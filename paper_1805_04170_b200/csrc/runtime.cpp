@@ -1312,6 +1312,8 @@ PlanRt::~PlanRt() {
   if (arena) cudaFree(arena);
 }
 
+static size_t lower_other_ranks(PlanRt& P);
+
 PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
   auto P = std::make_unique<PlanRt>();
   P->ctx = ctx;
@@ -1351,7 +1353,14 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
         ctx->comm = nccl_comm_init(1, uid, 0);
       }
     }
-    P->arena_bytes = std::max<size_t>(P->arena_used, kAlign);
+    // TPX_FLAG_PEER_SOLO: this rank alone, every peer's arena stood in for by its own (sized for
+    // the largest rank's layout): the rank's program runs unchanged with pulls reading local
+    // HBM instead of NVLink and the peer counters already satisfied -- one rank's compute and
+    // conversion time of an N-GPU step, measurable on one GPU (never a result: data is garbage)
+    const bool solo = P->peer() && (flags & 128) && ctx->world > 1;
+    if ((flags & 128) && !P->peer()) fail("TPX_FLAG_PEER_SOLO needs TPX_FLAG_PEER");
+    const size_t need = solo ? lower_other_ranks(*P) : P->arena_used;
+    P->arena_bytes = std::max<size_t>(need, kAlign);
     CUDA_CHECK(cudaMalloc(&P->arena, P->arena_bytes));
     // scratch padding (16-byte rows of im2col matrices, per-image column blocks) is read as
     // zero by the GEMMs and never written; the peer-mode sync counter starts at 0
@@ -1371,7 +1380,14 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
       P->sync.peer[ctx->rank] = P->sync.local;
       P->peer_base.assign(size_t(ctx->world), 0);
       P->peer_base[size_t(ctx->rank)] = P->base;
-      if (ctx->world > 1) return P.release();  // lowered by connect_peers once the arenas are mapped
+      if (solo) {
+        for (int r = 0; r < ctx->world; ++r) {
+          P->peer_base[size_t(r)] = P->base;
+          P->sync.peer[r] = P->sync.local;
+        }
+      } else if (ctx->world > 1) {
+        return P.release();  // lowered by connect_peers once the arenas are mapped
+      }
     }
     lower(*P, false);
     prepare_program(*P, P->main);
@@ -1384,6 +1400,35 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
     P->arena_bytes = P->arena_used;
   }
   return P.release();
+}
+
+// Every other rank's node values (and the largest arena any rank allocates), from a host-only
+// lowering of the plan as that rank (deterministic: the rank lowers exactly so itself).
+static size_t lower_other_ranks(PlanRt& P) {
+  const int world = P.ctx->world, me = P.ctx->rank;
+  P.rval.assign(size_t(world), {});
+  P.rval_b.assign(size_t(world), {});
+  P.rhas.assign(size_t(world), {});
+  size_t most = P.arena_used;
+  for (int r = 0; r < world; ++r) {
+    if (r == me) continue;
+    Ctx c2 = *P.ctx;
+    c2.rank = r;
+    c2.ordinal = -1;
+    PlanRt q;
+    q.ctx = &c2;
+    q.plan = P.plan;
+    q.precision = P.precision;
+    q.flags = P.flags;
+    q.esize = P.esize;
+    q.dev_rank = P.dev_rank;
+    lower(q, true);
+    most = std::max(most, q.arena_used);
+    P.rval[size_t(r)].swap(q.val);
+    P.rval_b[size_t(r)].swap(q.val_b);
+    P.rhas[size_t(r)].swap(q.has_val);
+  }
+  return most;
 }
 
 void arena_ipc_handle(PlanRt& P, void* out, size_t len) {
@@ -1411,27 +1456,7 @@ void connect_peers(PlanRt& P, const void* handles, size_t len) {
     P.peer_base[size_t(r)] = reinterpret_cast<uintptr_t>(ptr);
     P.sync.peer[r] = static_cast<const unsigned long long*>(ptr);
   }
-  // every other rank's node values, from a host-only lowering of the plan as that rank
-  P.rval.assign(size_t(world), {});
-  P.rval_b.assign(size_t(world), {});
-  P.rhas.assign(size_t(world), {});
-  for (int r = 0; r < world; ++r) {
-    if (r == me) continue;
-    Ctx c2 = *P.ctx;
-    c2.rank = r;
-    c2.ordinal = -1;
-    PlanRt q;
-    q.ctx = &c2;
-    q.plan = P.plan;
-    q.precision = P.precision;
-    q.flags = P.flags;
-    q.esize = P.esize;
-    q.dev_rank = P.dev_rank;
-    lower(q, true);
-    P.rval[size_t(r)].swap(q.val);
-    P.rval_b[size_t(r)].swap(q.val_b);
-    P.rhas[size_t(r)].swap(q.has_val);
-  }
+  lower_other_ranks(P);
   const size_t used = P.arena_used;
   lower(P, false);
   if (P.arena_used != used) fail("peer lowering is not deterministic");

@@ -32,6 +32,8 @@ FLAG_DIRECT_CONV = 4  # convolutions as direct CUDA-core loops (cross-check of t
 FLAG_GRAPH = 8        # the whole step replayed as one CUDA graph
 FLAG_LOOP = 16        # execute() = one training-loop step: the weights carry into the next step
 FLAG_PEER = 32        # cross-rank fetches pulled from the peers' arenas over NVLink (CUDA IPC)
+FLAG_KMAJOR_CONV = 64  # conv grad_input on transposed K-major operands (opt-in)
+FLAG_PEER_SOLO = 128  # one rank of an N-rank peer plan alone on this GPU (timing projection only)
 
 
 @dataclass

@@ -261,3 +261,28 @@ def test_bench_two_ranks_on_one_gpu():
     assert "peer pull" in d["config"]["exchange"]
     assert d["fetch_bytes_total"] > 0  # k = 1: the plan really crosses the rank boundary
     assert out.stderr.count("peer arenas of 2 ranks mapped") == 2
+
+
+@pytest.mark.parametrize("stem", [s for s in K12 if stem_id(s).startswith(("cfg1_mlp3x1024_b64.opt.k2", "mlp_train_d2.data.k2",
+                                                                          "alexr_conv_b4.opt.k1"))], ids=stem_id)
+def test_peer_solo_rank_runs(stem):
+    """TPX_FLAG_PEER_SOLO (bench's N-GPU projection): one rank of a 2^k-rank plan runs its program
+    alone on this GPU -- every launch, sync point and pull (reading its own arena) -- eagerly and as
+    a CUDA graph, without peers, errors or hangs; its pulled-byte count is the plan's."""
+    from paper_1805_04170_b200.executor import (FLAG_FUSE, FLAG_GRAPH, FLAG_LOOP, FLAG_PEER, FLAG_PEER_SOLO, Context,
+                                                PlanExecutor)
+    text, P, _, seed = load_golden(stem)
+    world = P["devices"]
+    for rk in (0, world - 1):
+        ctx = Context(0, rk, world)
+        for flags in (FLAG_FUSE | FLAG_PEER | FLAG_PEER_SOLO, FLAG_FUSE | FLAG_PEER | FLAG_PEER_SOLO | FLAG_GRAPH | FLAG_LOOP):
+            ex = PlanExecutor(ctx, text, flags=flags)
+            ex.init_inputs(seed)
+            for _ in range(3):
+                ex.execute()
+            ex.synchronize()
+            want = sum(n["bytes"] for n in P["nodes"] if n["kind"] == "fetch" and n["device"] == rk
+                       and n["src_device"] != rk)
+            assert ex.stats()["rank_xrank_bytes_in"] == want
+            ex.close()
+        ctx.close()
