@@ -728,8 +728,11 @@ struct Lowerer {
   }
 
   // ------------------------------------------------------------ conversions
+  // Class of same-rank copies: after the NCCL receives they may unpack (C_COPY); in peer mode
+  // there is no staging, so they share the phase's pull launch (C_XCHG): one launch, not two.
+  Cls copy_cls() const { return P.peer() ? C_XCHG : C_COPY; }
   void copy_into(const StridedView& dst, const StridedView& src) {
-    o_copy.descs.push_back(ndesc(NARY_COPY, dst, {src}));
+    (P.peer() ? o_pull : o_copy).descs.push_back(ndesc(NARY_COPY, dst, {src}));
   }
 
   void lower_fetch_or_slice(int ni) {
@@ -797,7 +800,7 @@ struct Lowerer {
         if (pending[size_t(src)] >= 0) produced(ni, Cls(pending[size_t(src)]));
         return;
       }
-      need(src, C_COPY);
+      need(src, copy_cls());
       const StridedView sv = subview(value(src), sn.region, n.region);
       if (cat >= 0) {
         ensure_alloc(cat);
@@ -806,7 +809,7 @@ struct Lowerer {
       } else {
         const StridedView d = set_val(ni, alloc(n.region.shape()));
         copy_into(d, sv);
-        produced(ni, C_COPY);
+        produced(ni, copy_cls());
       }
       return;
     }
@@ -856,11 +859,13 @@ struct Lowerer {
     ensure_alloc(ni);
     for (int s : n.sources) {
       if (defer_to[size_t(s)] == ni) continue;  // already pasted by the piece itself
-      need(s, C_COPY);
+      need(s, copy_cls());
       const PlanNode& pn = pl.nodes[size_t(s)];
       copy_into(subview(P.val[size_t(ni)], n.region, pn.region), value(s));
     }
-    produced(ni, C_COPY);
+    // (a concat whose pieces all landed by themselves -- pulls or copies -- is produced by
+    // the class that wrote them; the latest such class is the pull / copy one)
+    produced(ni, copy_cls());
   }
 
   void lower_reduce(int ni) {

@@ -18,7 +18,11 @@ for kv in filter(None, os.environ.get("TPX_GEMM_KNOBS", "").split(",")):  # gemm
 stem = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 text = gzip.open(os.path.join(ROOT, "plans", stem + ".plan.json.gz"), "rt").read()
-ex = PlanExecutor(Context(0), text, precision=0, flags=FLAG_FUSE | int(os.environ.get("TPX_EXTRA_FLAGS", "0")))
+# TPX_SOLO=rank,world: that rank of a world-rank peer plan alone (TPX_FLAG_PEER_SOLO timing)
+solo = os.environ.get("TPX_SOLO")
+ctx = Context(0, *[int(x) for x in solo.split(",")]) if solo else Context(0)
+ex = PlanExecutor(ctx, text, precision=0,
+                  flags=FLAG_FUSE | int(os.environ.get("TPX_EXTRA_FLAGS", "0")) | (32 | 128 if solo else 0))
 ex.init_inputs(7)
 for _ in range(3):
     ex.execute()
