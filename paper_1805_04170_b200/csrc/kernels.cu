@@ -160,12 +160,14 @@ __device__ __forceinline__ bool peer_wait_one(const unsigned long long* p, unsig
                                               unsigned long long timeout_ns, int r) {
   if (ld_acquire_sys(p) >= c) return true;
   const unsigned long long t0 = globaltimer();
-  while (ld_acquire_sys(p) < c) {
-    if (*reinterpret_cast<volatile int*>(err)) return false;
-    __nanosleep(200);
-    if (globaltimer() - t0 > timeout_ns) {
-      atomicExch(err, 0x100 | r);
-      return false;
+  for (unsigned spins = 1; ld_acquire_sys(p) < c; ++spins) {
+    __nanosleep(100);
+    if ((spins & 255u) == 0) {  // (the error word is host memory: read it rarely)
+      if (*reinterpret_cast<volatile int*>(err)) return false;
+      if (globaltimer() - t0 > timeout_ns) {
+        atomicExch(err, 0x100 | r);
+        return false;
+      }
     }
   }
   return true;
@@ -177,16 +179,39 @@ __device__ __forceinline__ void peer_wait(const PeerSync& s, uint32_t mask, unsi
     if ((mask >> r & 1u) && !peer_wait_one(s.peer[r], c, s.err, s.timeout_ns, r)) return;
 }
 
-__global__ void sync_kernel(PeerSync s, int barrier) {
-  if (threadIdx.x != 0) return;
+__device__ __forceinline__ void peer_publish(const PeerSync& s, unsigned long long v) {
   // everything earlier on this stream (previous launches) is complete: publish it
-  const unsigned long long c = *s.local + 1;
-  // the release store orders every write that happens-before it (earlier launches on this
-  // stream included) for observers at system scope; fence.acq_rel.sys is the lighter fence
-  // (a fence.sc.sys measured ~8 us per signal)
   asm volatile("fence.acq_rel.sys;" ::: "memory");
-  st_release_sys(s.local, c);
-  if (barrier) peer_wait(s, ((1u << s.world) - 1u) & ~(1u << s.rank), c);
+  st_release_sys(s.local, v);
+}
+// the value sync point `idx` of the current step publishes (-1: the previous barrier's)
+__device__ __forceinline__ unsigned long long sync_value(const PeerSync& s, int idx) {
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(s.epoch);
+  // (+ 1: the counters start at 0, and the first point of the first step must not be satisfied
+  // before it is published)
+  return idx >= 0 ? e * kSyncK + unsigned(idx) + 1ull : e * kSyncK - 1ull;
+}
+
+__global__ void sync_kernel(PeerSync s, int index, int barrier) {
+  if (threadIdx.x != 0) return;
+  if (!barrier) {
+    peer_publish(s, sync_value(s, index));
+    return;
+  }
+  const unsigned long long e = *s.epoch, v = e * kSyncK + (kSyncK - 1ull);
+  peer_publish(s, v);
+  peer_wait(s, ((1u << s.world) - 1u) & ~(1u << s.rank), v);
+  *s.epoch = e + 1;  // read only by this rank's later launches (stream order)
+}
+
+// Start of a conversion launch in peer mode: publish the phase's sync point (every block writes
+// the same value: idempotent) and wait for the ranks this block reads from.
+// (block 0 publishes -- any block starts after everything earlier on the stream; a rank never
+// waits on itself: its own data is ordered by the stream)
+__device__ __forceinline__ void peer_prologue(const PeerSync& s, int signal_s, int wait_s, uint32_t mask) {
+  if (signal_s >= 0 && blockIdx.x == 0) peer_publish(s, sync_value(s, signal_s));
+  mask &= ~(1u << s.rank);
+  if (mask) peer_wait(s, mask, sync_value(s, wait_s));
 }
 
 // Chained elementwise stage (EpiOp codes, gemm.h) on the previous stage's stored value.
@@ -211,7 +236,7 @@ __device__ __forceinline__ float stored(float v) {
 // descriptor table costs dozens of dependent loads per block).
 template <class T>
 __global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
-                                                           PeerSync sync) {
+                                                           PeerSync sync, int signal_s, int wait_s) {
   __shared__ __align__(16) unsigned char sraw[(sizeof(NaryDev) + 15) / 16 * 16];
   __shared__ int sdi;
   if (threadIdx.x == 0) sdi = __ldg(tile_desc + blockIdx.x);
@@ -224,8 +249,8 @@ __global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __rest
   __syncthreads();
   const NaryDev& D = *reinterpret_cast<const NaryDev*>(sraw);
   const NaryDesc& d = D.d;
-  if (d.wait_mask) {  // peer pull: the sources on other ranks must be complete
-    if (threadIdx.x == 0) peer_wait(sync, d.wait_mask, *sync.local);
+  if (d.wait_mask || signal_s >= 0) {  // peer mode: publish the phase, wait for the sources' ranks
+    if (threadIdx.x == 0) peer_prologue(sync, signal_s, wait_s, d.wait_mask);
     __syncthreads();
   }
   const int64_t local = int64_t(blockIdx.x) - d.tile_begin;
@@ -353,12 +378,12 @@ __global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __rest
 // loads in flight per thread -- enough to cover NVLink latency on a peer read.
 template <class T>
 __global__ void __launch_bounds__(kThreads, 3) copy_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
-                                                           PeerSync sync) {
+                                                           PeerSync sync, int signal_s, int wait_s) {
   __shared__ int sdi;
   if (threadIdx.x == 0) {
     const int di = __ldg(tile_desc + blockIdx.x);
     sdi = di;
-    if (ds[di].d.wait_mask) peer_wait(sync, ds[di].d.wait_mask, *sync.local);
+    if (ds[di].d.wait_mask || signal_s >= 0) peer_prologue(sync, signal_s, wait_s, ds[di].d.wait_mask);
   }
   __syncthreads();
   const NaryDev& D = ds[sdi];
@@ -926,17 +951,20 @@ void nary_prepare(NaryBatch& b) {
 }
 
 void nary_run(const NaryBatch& b, cudaStream_t s) {
-  if (!b.tiles) return;
+  if (!b.tiles) {
+    if (b.signal_s >= 0) sync_signal(b.sync, b.signal_s, false, s);  // nothing to move: still publish
+    return;
+  }
   const NaryDev* ds = static_cast<const NaryDev*>(b.d_descs);
   const int* td = static_cast<const int*>(b.d_tile_desc);
   if (b.copy_only) {
-    if (b.bf16) copy_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
-    else copy_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
+    if (b.bf16) copy_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
+    else copy_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
     CUDA_CHECK(cudaGetLastError());
     return;
   }
-  if (b.bf16) nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
-  else nary_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync);
+  if (b.bf16) nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
+  else nary_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
   CUDA_CHECK(cudaGetLastError());
 }
 
@@ -949,8 +977,8 @@ void numeric_check_run(const NaryBatch& b, unsigned* dev_out, cudaStream_t s) {
   CUDA_CHECK(cudaGetLastError());
 }
 
-void sync_signal(const PeerSync& s, bool barrier, cudaStream_t st) {
-  sync_kernel<<<1, 32, 0, st>>>(s, barrier ? 1 : 0);
+void sync_signal(const PeerSync& s, int index, bool barrier, cudaStream_t st) {
+  sync_kernel<<<1, 32, 0, st>>>(s, index, barrier ? 1 : 0);
   CUDA_CHECK(cudaGetLastError());
 }
 

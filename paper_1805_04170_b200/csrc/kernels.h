@@ -72,25 +72,33 @@ struct NaryDesc {
   uint32_t wait_mask;   // peer pull: ranks whose sync counter must reach this rank's first
 };
 
-// Cross-rank ordering of peer-pull steps (TPX_FLAG_PEER).  Every rank owns one 64-bit sync
-// counter at the start of its arena; the other ranks map that arena (CUDA IPC over NVLink).
-// A signal step bumps the local counter after everything earlier on the stream; a pull waits
-// until each rank it reads from has reached the local count (acquire at system scope), so the
-// data it reads is complete.  A barrier (signal + wait for every rank) ends each step, so no
-// rank overwrites a value another rank may still be reading.
+// Cross-rank ordering of peer-pull steps (TPX_FLAG_PEER).  Every rank owns two 64-bit words at
+// the start of its arena: a counter the other ranks read (they map the arena, CUDA IPC over
+// NVLink) and its step epoch E (the barriers it has passed).  At sync point s of a step -- the
+// first conversion launch of a phase in which any rank pulls -- every rank publishes
+// E * kSyncK + s + 1 (fence + st.release.sys, from any launch that runs after the phase's producers:
+// the phase's own pull / reduce launch, or a one-thread kernel when the rank has none); a pull
+// waits until each rank it reads from has published at least that value (ld.acquire.sys), so the
+// data it reads is complete.  A barrier ends each step (E * kSyncK + kSyncK - 1 from every rank,
+// then E + 1), so no rank overwrites a value another rank may still read; a pull of the carry
+// program, which runs right after a barrier, waits for the previous barrier's value.
+constexpr unsigned long long kSyncK = 1ull << 20;
 struct PeerSync {
-  unsigned long long* local = nullptr;
+  unsigned long long* local = nullptr;  // this rank's counter (arena word 0)
+  unsigned long long* epoch = nullptr;  // this rank's step epoch (arena word 1)
   const unsigned long long* peer[kMaxRanks] = {};
   int* err = nullptr;                   // host-mapped: 0x100 | rank on a wait that timed out
   int world = 1, rank = 0;
   unsigned long long timeout_ns = 0;
 };
-void sync_signal(const PeerSync& s, bool barrier, cudaStream_t st);
+void sync_signal(const PeerSync& s, int index, bool barrier, cudaStream_t st);
 
 struct NaryBatch {
   bool bf16 = false;  // storage type of every operand (arithmetic is fp32)
   bool pull = false;  // some descriptor reads peer memory (waits on PeerSync first)
   bool copy_only = false;  // every descriptor a plain copy: the light copy kernel (nary_prepare)
+  int signal_s = -1;  // peer mode: this launch publishes sync point signal_s (see PeerSync)
+  int wait_s = -1;    // ... and its pulls wait for the peers' sync point wait_s (-1: last barrier)
   void* d_tile_desc = nullptr;  // int32 per block: its descriptor (no per-block search)
   PeerSync sync;
   std::vector<NaryDesc> descs;

@@ -193,10 +193,20 @@ struct Lowerer {
     v.ptr = reinterpret_cast<float*>(P.peer_base[size_t(r)] + (reinterpret_cast<uintptr_t>(v.ptr) - kFakeBase));
     return v;
   }
+  // Peer-mode sync points: a phase's signal is published by its first conversion launch on this
+  // rank (or a one-thread launch when the rank has none); its pulls wait for the peers' value of
+  // the same point.  Barriers are their own launch.
+  int sync_idx = 0;            // next sync point index of this program
+  int pending_signal = -1;     // sync point not yet attached to a launch
+  int phase_sync = -1;         // sync point of the open phase (pull wait target; -1: last barrier)
   void sync_step(bool barrier) {
     flush();
-    const int s = add_step(ST_SYNC, 0, barrier ? std::string() : seg_op, barrier ? "barrier" : "signal");
-    prog.steps[size_t(s)].barrier = barrier ? 1 : 0;
+    if (!barrier) {
+      pending_signal = phase_sync = sync_idx++;
+      return;
+    }
+    const int s = add_step(ST_SYNC, -1, std::string(), "barrier");
+    prog.steps[size_t(s)].barrier = 1;
   }
 
   int rank_of(int dev) const { return P.dev_rank[size_t(dev)]; }
@@ -215,6 +225,11 @@ struct Lowerer {
   void flush() {
     auto emit_nary = [&](NaryBatch& b, const std::string& op, const std::string& what, Cls c) {
       if (b.descs.empty()) return;
+      if (c >= C_PACK && pending_signal >= 0) {  // the phase's first conversion launch publishes it
+        b.signal_s = pending_signal;
+        pending_signal = -1;
+      }
+      if (b.pull) b.wait_s = phase_sync;
       prog.nary.push_back(std::move(b));
       b = NaryBatch{};
       const int s = add_step(ST_NARY, int(prog.nary.size()) - 1, op, what);
@@ -249,7 +264,7 @@ struct Lowerer {
     }
     post_open.clear();
     emit_nary(o_pack, seg_op, "pack", C_PACK);
-    if (!o_pull.descs.empty()) o_pull.pull = true;
+    for (const auto& d : o_pull.descs) o_pull.pull = o_pull.pull || d.wait_mask != 0;  // (local copies share it)
     emit_nary(o_pull, seg_op, "pull", C_XCHG);
     if (!o_xchg.x.empty()) {
       prog.xchg.push_back(std::move(o_xchg));
@@ -260,6 +275,11 @@ struct Lowerer {
     emit_nary(o_copy, seg_op, "copy", C_COPY);
     const bool had_reduce = !o_reduce.descs.empty();
     emit_nary(o_reduce, seg_op, "reduce", C_REDUCE);
+    if (pending_signal >= 0) {  // no conversion launch on this rank at this sync point
+      const int s = add_step(ST_SYNC, pending_signal, seg_op, "signal");
+      prog.steps[size_t(s)].barrier = 0;
+      pending_signal = -1;
+    }
     if (had_reduce) {
       for (int r : open_red) {
         RedTail& t = red_tail[r];
@@ -1037,6 +1057,7 @@ struct Lowerer {
         seg_op = op_of_phase(n.phase);
         seen_conv = false;
         synced = false;
+        phase_sync = -1;
       }
       if (!synced && n.kind != NodeKind::sub_op && n.kind != NodeKind::buffer && xph.count(n.phase)) {
         sync_step(false);  // after this phase's compute, before any of its pulls
@@ -1273,14 +1294,15 @@ void lower(PlanRt& P, bool dry) {
     L.run_carry();
   }
   P.n_sync = 0;
-  for (const auto& st : P.main.steps) P.n_sync += st.kind == ST_SYNC;
+  for (const auto& st : P.main.steps)
+    P.n_sync += st.kind == ST_SYNC || (st.kind == ST_NARY && P.main.nary[size_t(st.idx)].signal_s >= 0);
 }
 
 void prepare_program(PlanRt& P, Program& prog) {
   const bool bf = P.esize == 2;
   for (auto& b : prog.nary) {
     b.bf16 = bf;
-    if (b.pull) b.sync = P.sync;
+    if (b.pull || b.signal_s >= 0) b.sync = P.sync;
     nary_prepare(b);
   }
   for (auto& b : prog.conv) {
@@ -1377,6 +1399,7 @@ PlanRt* load_plan(Ctx* ctx, const std::string& json, int precision, int flags) {
       int* err_dev = nullptr;
       CUDA_CHECK(cudaHostGetDevicePointer(&err_dev, P->err_host, 0));
       P->sync.local = reinterpret_cast<unsigned long long*>(P->arena);
+      P->sync.epoch = reinterpret_cast<unsigned long long*>(P->arena) + 1;
       P->sync.err = err_dev;
       P->sync.world = ctx->world;
       P->sync.rank = ctx->rank;
@@ -1506,7 +1529,7 @@ static void launch_step(PlanRt& P, Program& prog, const Step& s, cudaStream_t st
     case ST_NARY: nary_run(prog.nary[size_t(s.idx)], st); break;
     case ST_GEMM: gemm_run(prog.gemm[size_t(s.idx)], st); break;
     case ST_CONV: conv_run(prog.conv[size_t(s.idx)], st); break;
-    case ST_SYNC: sync_signal(P.sync, s.barrier != 0, st); break;
+    case ST_SYNC: sync_signal(P.sync, s.idx, s.barrier != 0, st); break;
     case ST_XCHG: {
       const XchgGroup& g = prog.xchg[size_t(s.idx)];
       nccl_group_start();
@@ -1849,7 +1872,7 @@ std::string describe(const PlanRt& P) {
           mask |= d.wait_mask;
         }
         s << ",\"bytes\":" << int64_t(bytes) << ",\"chained\":" << chained << ",\"pull\":" << (b.pull ? 1 : 0)
-          << ",\"wait_mask\":" << mask;
+          << ",\"wait_mask\":" << mask << ",\"signal\":" << b.signal_s << ",\"wait_s\":" << b.wait_s;
       } else if (st.kind == ST_GEMM) {
         const auto& specs = prog.gemm_specs[size_t(st.idx)];
         s << ",\"problems\":" << specs.size() << ",\"shapes\":[";
@@ -1888,7 +1911,7 @@ std::string describe(const PlanRt& P) {
         s << ",\"descs\":" << prog.conv[size_t(st.idx)].descs.size()
           << ",\"bytes\":" << int64_t(prog.conv[size_t(st.idx)].bytes);
       } else if (st.kind == ST_SYNC) {
-        s << ",\"barrier\":" << st.barrier;
+        s << ",\"barrier\":" << st.barrier << ",\"signal\":" << (st.barrier ? -1 : st.idx);
       }
       s << "}";
     }

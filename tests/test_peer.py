@@ -26,7 +26,15 @@ MULTI = [s for s in STEMS if int(stem_id(s).split(".k")[1].split(".")[0]) >= 1]
 
 
 def sync_sequence(desc, prog="main"):
-    return [(s["op"], s["barrier"]) for s in desc[prog]["steps"] if s["kind"] == "sync"]
+    """Sync points in launch order: a signal folded into a phase's first conversion launch or a
+    one-thread signal launch (its index), or a barrier ("B")."""
+    out = []
+    for s in desc[prog]["steps"]:
+        if s["kind"] == "sync":
+            out.append("B" if s["barrier"] else s["signal"])
+        elif s["kind"] == "nary" and s.get("signal", -1) >= 0:
+            out.append(s["signal"])
+    return out
 
 
 @pytest.mark.parametrize("stem", MULTI, ids=stem_id)
@@ -54,8 +62,11 @@ def test_peer_lowering_bytes_and_sync(stem):
         assert all(q == seqs[0] for q in seqs), "ranks disagree on the sync points"
         xphases = {n["phase"] for n in P["nodes"]
                    if n["kind"] == "fetch" and dev_rank(n["device"]) != dev_rank(n["src_device"])}
-        assert len([q for q in seqs[0] if not q[1]]) == len(xphases)
-        assert (seqs[0][-1][1] == 1) if xphases else not seqs[0]
+        assert seqs[0] == (list(range(len(xphases))) + ["B"] if xphases else [])
+        for r, d in enumerate(descs):  # every pull waits for its own phase's sync point
+            for s in d["main"]["steps"]:
+                if s["kind"] == "nary" and s.get("pull"):
+                    assert 0 <= s["wait_s"] < len(xphases)
         for r, d in enumerate(descs):
             steps = d["main"]["steps"]
             assert not [s for s in steps if s["kind"] == "nccl"]
@@ -123,4 +134,5 @@ def test_peer_loop_mode_carry_has_barrier(stem):
     carry = [sync_sequence(d, "carry") for d in descs]
     assert carry[0] == carry[1]
     if any(s["kind"] == "nary" and s.get("pull") for d in descs for s in d["carry"]["steps"]):
-        assert carry[0] and carry[0][-1][1] == 1
+        assert carry[0] == ["B"]  # the carry's pulls wait for the main program's barrier
+        assert all(s["wait_s"] == -1 for d in descs for s in d["carry"]["steps"] if s["kind"] == "nary" and s.get("pull"))
