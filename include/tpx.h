@@ -208,6 +208,10 @@ int tpx_gemm_schedule(int nprob, int P, int Q, int K, int bn, int num_sms, int f
  *   stream_k, group, tstore (TMA-store epilogue), nbox, odepth, stages, units (CTAs), split
  *   (3xTF32), bf16. */
 int tpx_gemm_last_launch(int64_t* info, int n);
+/* Debug: per-CTA launch timeline of the last GEMM launched with knob (22, 1) (8 %globaltimer
+ * stamps per CTA: entry, setup, first TMA, first k-block landed, MMA done, first accumulator,
+ * epilogue done, exit); fills min(n, 320 * 8) values. */
+int tpx_debug_gemm_trace(uint64_t* out, int n);
 /* Debug: override the MN-major UMMA descriptor strides (bytes; 0 = defaults). */
 int tpx_debug_gemm_mn_desc(unsigned lbo, unsigned sbo);
 

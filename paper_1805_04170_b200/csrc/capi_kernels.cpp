@@ -159,6 +159,10 @@ __attribute__((visibility("default"))) int tpx_gemm_last_launch(int64_t* info, i
   });
 }
 
+__attribute__((visibility("default"))) int tpx_debug_gemm_trace(uint64_t* out, int n) {
+  return tpx::guard([&] { tpx::gemm_debug_trace(reinterpret_cast<unsigned long long*>(out), n); });
+}
+
 __attribute__((visibility("default"))) int tpx_debug_gemm_mn_desc(unsigned lbo, unsigned sbo) {
   tpx::gemm_debug_mn_desc(lbo, sbo);
   return 0;

@@ -50,6 +50,17 @@ constexpr int kSegQ = 8;  // tile queue depth (dynamic schedules)
 
 enum SegKind : int { SEG_WHOLE = 0, SEG_HEAD = 1, SEG_PART = 2 };
 
+// debug (22, 1): per-CTA timeline of one launch (%globaltimer, ns) at 8 milestones:
+// entry, setup done, first TMA issued, first k-block landed (MMA), MMA loop done, first
+// accumulator ready (epilogue), epilogue done, exit.
+__device__ unsigned long long g_gemm_trace[320][8];
+__device__ __forceinline__ void trace_mark(bool on, int i) {
+  if (!on) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_gemm_trace[blockIdx.x < 320 ? blockIdx.x : 319][i] = t;
+}
+
 __host__ __device__ constexpr uint32_t operand_bytes(int bn) { return uint32_t(BM * BK * 4 + bn * BK * 4); }
 __host__ __device__ constexpr uint32_t stage_bytes(int bn, bool split) {
   return operand_bytes(bn) * (split ? 2u : 1u);
@@ -416,6 +427,16 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   // handed out in order by flags[0] (flags[1] counts finished units, the last one resets both)
   const int s_begin = dyn ? 0 : seg_off[unit], s_end = dyn ? seg_off[1] : seg_off[unit + 1];
   const int warp = warp_id(), lane = lane_id();
+  const bool tr = (has_other >> 16) & 1;
+  if (threadIdx.x == 0) trace_mark(tr, 0);
+  if (warp == 3 && lane == 0 && !dyn && s_begin < s_end) {
+    // the first segment's operand descriptors, fetched while the CTA sets up (a cold tensor map
+    // costs the producer's first TMA a global round trip)
+    const GemmProblem& p0 = probs[segs[s_begin].prob];
+    tma_prefetch_desc(p0.tmap_a);
+    tma_prefetch_desc(p0.tmap_b);
+    if (p0.tmap_other) tma_prefetch_desc(p0.tmap_other);
+  }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -448,6 +469,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) trace_mark(tr, 1);
   // the leader's barriers, as shared::cluster addresses (pair TMA and epilogue arrivals)
   const uint32_t full_lead = PAIR ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
   const uint32_t tmem_empty_lead = PAIR ? mapa_shared(smem_u32(tmem_empty), 0) : smem_u32(tmem_empty);
@@ -539,6 +561,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         // the leader's full barrier expects both CTAs' bytes; the peer's TMA completes on it
         if (rank == 0) mbar_arrive_expect_tx(&full[s], PAIR ? 2 * OPB : OPB);
         load_kblock(pr, kb, p0, q0, sa, sa + A_BYTES, &full[s], full_lead + s * 8, pol_a, pol_b);
+        if (j == 0 && kb == sg.kb0) trace_mark(tr, 2);
       }
     }
   } else if (warp == 1 && lane == 0 && rank == 0) {
@@ -563,6 +586,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       for (int kb = ck0; kb < ck1; ++kb, (++s == uint32_t(STAGES)) ? (s = 0, ph ^= 1) : 0) {
         if constexpr (SPLIT) mbar_wait(&split_done[s], ph);
         else mbar_wait(&full[s], ph);
+        if (ai == 1 && kb == ck0) trace_mark(tr, 3);
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * STAGE);
         const uint32_t sb = sa + A_BYTES;
@@ -601,6 +625,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       else mma_commit(&tmem_full[acc]);
       }
     }
+    trace_mark(tr, 4);
   } else if (warp == 3 && lane == 0 && oload) {
     // ---------------- operand loader: the epilogue's elementwise operand (w of
     // w_next = w - wd) as one 32 x 32 box per TMEM lane quarter and 32-column step (the two
@@ -774,6 +799,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       const uint32_t taddr = tmem_base + acc * BN + (uint32_t(lq * 32) << 16);
       if (has_other & 2) mbar_wait_sleep(&tmem_full[acc], aph);
       else mbar_wait(&tmem_full[acc], aph);
+      if (ew == 0 && lane == 0 && ai == 1) trace_mark(tr, 5);
       tc_fence_after();
 
       if (sg.kind == SEG_PART) {
@@ -1148,6 +1174,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     }
   }
   if (warp >= 4 && warp < 4 + NEPI && lane == 0) bulk_wait<0>();  // TMA-store epilogue drained
+  if (warp == 4 && lane == 0) trace_mark(tr, 6);
   tc_fence_before();
   if constexpr (PAIR) cluster_sync();  // both CTAs done with the pair's TMEM and barriers
   else __syncthreads();
@@ -1160,6 +1187,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       __threadfence();
     }
   }
+  if (threadIdx.x == 0) trace_mark(tr, 7);
   if (warp == 2) {
     tc_fence_after();
     if constexpr (PAIR) tmem_dealloc_pair(tmem_base, TMEM_COLS);
@@ -1222,6 +1250,9 @@ bool g_no_dyn = true;  // whole-tile schedules from a device tile counter: opt-i
 int g_odepth = 0;      // debug (15, n): operand ring depth n (0 = chosen from the smem budget)
 int g_min_stages = 4;  // debug (16, n): mainloop stages the operand ring must leave
 int g_ts_chain = 0;    // debug (18, n): TMA-store epilogue also for chains (n = 1 single, 2 double-buffered boxes)
+int g_trace = 0;       // debug (22, 1): per-CTA launch timeline (tpx_debug_gemm_trace)
+int g_whole = 0;       // debug (23, 1): whole tiles whenever there are no more tiles than groups
+int g_defer = 0;       // debug (24, 1): deferred stream-K fixup launch instead of in-kernel heads (measured slower: off)
 int g_rr_tiles = 1;    // debug (20, n): whole-tile schedules dealt round-robin (1, default) or in contiguous blocks (0)
 int g_tq_block = 0;    // debug (21, n): tile list in blocks of n Q-tiles (0 = Q-tile major)
 
@@ -1305,6 +1336,10 @@ struct SchedPiece { int group, kb0, kb1; };
 
 }  // namespace
 
+void gemm_debug_trace(unsigned long long* out, int n) {
+  CUDA_CHECK(cudaMemcpyFromSymbol(out, g_gemm_trace, size_t(std::min(n, 320 * 8)) * 8));
+}
+
 void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   g_dbg_lbo = lbo;
   g_dbg_sbo = sbo;
@@ -1326,9 +1361,12 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 15) g_odepth = int(sbo);             // (15,n) epilogue operand ring depth n
   if (lbo == 16) g_min_stages = int(sbo);         // (16,n) keep >= n mainloop stages
   if (lbo == 18) g_ts_chain = int(sbo);           // (18,n) TMA-store chain epilogues
+  if (lbo == 22) g_trace = int(sbo);              // (22,1) launch timeline
+  if (lbo == 23) g_whole = int(sbo);              // (23,1) whole tiles instead of stream-K
+  if (lbo == 24) g_defer = int(sbo);              // (24,n) deferred stream-K fixup
   if (lbo == 20) g_rr_tiles = int(sbo);           // (20,n) round-robin whole tiles
   if (lbo == 21) g_tq_block = int(sbo);           // (21,n) Q-tile blocks in the tile list
-  if (lbo >= 1 && lbo <= 21) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
+  if (lbo >= 1 && lbo <= 24) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1343,7 +1381,7 @@ bool gemm_view_ok(const MatView& v, bool bf16) {
 // (column, k-block); each group gets a contiguous, equal share of the units (stream-K) or, when
 // there are plenty of columns, a contiguous run of whole columns.
 GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int num_sms,
-                           int force_groups, int max_kb) {
+                           int force_groups, int max_kb, bool deferred) {
   GemmSchedule S;
   if (probs.empty()) return S;
   // group width: the P-tile count of small-M problems whose Q operand is large (streamed)
@@ -1392,7 +1430,7 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
   // fp32-accurate at any K (K = 8192: 4e-5 -> ~1e-6 normwise).
   bool chunked = false;
   for (const auto& c : cols) chunked = chunked || (max_kb > 0 && c.kb > max_kb);
-  const bool whole = !chunked && (ncols >= 8 * groups || ncols % groups == 0);
+  const bool whole = !chunked && (ncols >= 8 * groups || ncols % groups == 0 || (g_whole && ncols <= groups));
   if (whole) groups = std::min(groups, ncols);
 
   // pieces[col] = ordered (group, kb0, kb1)
@@ -1445,7 +1483,8 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
       }
     }
   }
-  // slots: one per non-head piece per P-tile lane
+  // slots: one per non-head piece per P-tile lane (deferred: one per piece, the head's first)
+  deferred = deferred && !chunked && !whole;
   std::vector<int> slot_base(size_t(ncols) * size_t(G), -1);
   int nslots = 0;
   for (int c = 0; c < ncols; ++c) {
@@ -1453,9 +1492,12 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
     if (np <= 1) continue;
     for (int j = 0; j < cols[size_t(c)].ntp; ++j) {
       slot_base[size_t(c) * G + j] = nslots;
-      nslots += np - 1;
+      nslots += deferred ? np : np - 1;
+      if (deferred)
+        S.fixups.push_back({cols[size_t(c)].prob, cols[size_t(c)].tp0 + j, cols[size_t(c)].tq, slot_base[size_t(c) * G + j], np});
     }
   }
+  S.deferred = deferred;
   S.grid = groups * G;
   S.seg_off.assign(size_t(S.grid) + 1, 0);
   for (int g = 0; g < groups; ++g) {
@@ -1474,6 +1516,9 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
         sg.kb1 = pc.kb1;
         if (ps.size() == 1) {
           sg.kind = SEG_WHOLE;
+        } else if (deferred) {  // every piece a partial slot, in k order from the head's
+          sg.kind = SEG_PART;
+          sg.slot = slot_base[size_t(cp.first) * G + j] + cp.second;
         } else if (cp.second == 0) {
           sg.kind = SEG_HEAD;
           sg.slot = slot_base[size_t(cp.first) * G + j];
@@ -1680,6 +1725,24 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     }
   }
   g.sched = gemm_schedule(probs, g.bn, g.pair ? num_sms / 2 : num_sms, 0, split ? g_split_kb : 0);
+  if (g.sched.stream_k && g_defer && !split && !bf) {
+    // deferred fixup: row-major outputs whose epilogue views share the product's layout, and at
+    // most kMaxIn pieces per tile (the fixup is one ordered n-ary sum + the chain)
+    bool ok = g.bn % 4 == 0;
+    for (const auto& pr : probs) {
+      ok = ok && pr.out_cs == 1 && pr.Q % 4 == 0;
+      for (int e = 0; e < pr.n_epi; ++e)
+        ok = ok && pr.epi[e].out_cs == 1 && pr.epi[e].out_rs == pr.out_rs &&
+             (!pr.epi[e].other || (pr.epi[e].o_cs == 1 && pr.epi[e].o_rs == pr.out_rs));
+    }
+    int most = 0;
+    for (int c = 0, i = 0; i < int(g.sched.segs.size()); ++i) {
+      (void)c;
+      if (g.sched.segs[size_t(i)].kind == SEG_HEAD) most = std::max(most, g.sched.segs[size_t(i)].n_parts + 1);
+    }
+    if (ok && most <= kMaxIn)
+      g.sched = gemm_schedule(probs, g.bn, g.pair ? num_sms / 2 : num_sms, 0, 0, true);
+  }
   if (!g.sched.stream_k && !g_no_dyn) {
     // Whole tiles only: hand them out in order from a device counter instead of fixed per-CTA
     // lists, so SMs that run ahead (less contention, nearer memory) take more tiles and the
@@ -1714,6 +1777,44 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
   } else if (g.sched.dynamic) {
     CUDA_CHECK(cudaMalloc(&g.d_flags, 2 * sizeof(unsigned)));  // tile counter, finished units
     CUDA_CHECK(cudaMemset(g.d_flags, 0, 2 * sizeof(unsigned)));
+  }
+  if (g.sched.deferred) {
+    // per cut tile (and CTA half of a pair tile): out = sum of its k-ordered partial slots, then
+    // the problem's epilogue chain -- rows walked fastest so the slot reads are coalesced
+    const int PBM = g.pair ? 2 * BM : BM;
+    for (const auto& f : g.sched.fixups) {
+      const GemmProblem& pr = probs[size_t(f.prob)];
+      for (int half = 0; half < (g.pair ? 2 : 1); ++half) {
+        const long long r0 = (long long)f.tp * PBM + half * BM, c0 = (long long)f.tq * g.bn;
+        if (r0 >= pr.P || c0 >= pr.Q) continue;
+        const long long nr = std::min<long long>(BM, pr.P - r0), nc = std::min<long long>(g.bn, pr.Q - c0);
+        auto view3 = [&](const float* base, long long st_c4, long long st_r) {
+          StridedView v;
+          v.ptr = const_cast<float*>(base);
+          v.rank = 3;
+          v.shape[0] = nc / 4; v.shape[1] = nr; v.shape[2] = 4;
+          v.st[0] = st_c4; v.st[1] = st_r; v.st[2] = 1;
+          return v;
+        };
+        const StridedView out = view3(pr.out + r0 * pr.out_rs + c0, 4, pr.out_rs);
+        std::vector<StridedView> parts;
+        for (int i = 0; i < f.n_parts; ++i) {
+          const long long slot = (long long)(g.pair ? 2 * (f.slot0 + i) + half : f.slot0 + i);
+          parts.push_back(view3(g.d_ws + slot * BM * g.bn, 4LL * BM, 4));
+        }
+        NaryDesc d = nary_desc(NARY_SUM, out, parts, 0.f, 4);
+        for (int e = 0; e < pr.n_epi; ++e) {
+          const EpiStage& st = pr.epi[e];
+          const StridedView eo = view3(st.out + r0 * st.out_rs + c0, 4, st.out_rs);
+          StridedView ot;
+          if (st.other) ot = view3(st.other + r0 * st.o_rs + c0, 4, st.o_rs);
+          if (!nary_add_chain(d, out, st.op, st.scale, eo, st.other ? &ot : nullptr, 4))
+            throw std::runtime_error("gemm: deferred fixup cannot chain the epilogue");
+        }
+        g.fixup.descs.push_back(d);
+      }
+    }
+    nary_prepare(g.fixup);
   }
   const size_t nload = maps.size();
   maps.insert(maps.end(), store_maps.begin(), store_maps.end());
@@ -1762,7 +1863,7 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair, g.bf16);
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
-  const int flags = (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
+  const int flags = (g_trace ? 1 << 16 : 0) | (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
                     (g.other_smem && g.oloader && !g.sched.dynamic ? 2048 : 0) | (g.split ? (g_split_chain & 15) << 12 : 0);
   if (g.pair) {
     cudaLaunchConfig_t cfg = {};
@@ -1784,9 +1885,11 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
                                                           g.stages, g.prefetch, flags);
   }
   CUDA_CHECK(cudaGetLastError());
+  if (g.sched.deferred) nary_run(g.fixup, stream);
 }
 
 void gemm_free(GemmLaunch& g) {
+  nary_free(g.fixup);
   if (g.d_problems) cudaFree(g.d_problems);
   if (g.d_tmaps) cudaFree(g.d_tmaps);
   if (g.d_ws) cudaFree(g.d_ws);

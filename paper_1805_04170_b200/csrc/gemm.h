@@ -12,6 +12,8 @@
 
 #include <cuda_runtime.h>
 
+#include "kernels.h"
+
 namespace tpx {
 
 enum EpiOp : int {
@@ -77,6 +79,14 @@ struct GemmSchedule {
   std::vector<GemmSeg> segs;    // all CTAs' lists, concatenated
   std::vector<int> seg_off;     // CTA c owns segs[seg_off[c], seg_off[c+1])
   bool dynamic = false;         // segs handed out in order by a device counter (seg_off = {0, n})
+  // deferred fixup: every piece of a cut tile (its head too) writes a partial slot; a following
+  // launch sums each tile's slots in k order and runs the epilogue chain, spread over the GPU,
+  // instead of one head CTA per tile doing it serially at the end of the kernel
+  bool deferred = false;
+  struct Fixup {
+    int prob, tp, tq, slot0, n_parts;
+  };
+  std::vector<Fixup> fixups;
 };
 
 // Host-side description of one sub-op matmul over strided row-major fp32 views.
@@ -121,6 +131,7 @@ struct GemmLaunch {
   size_t ws_floats = 0;
   size_t smem_bytes = 0;
   std::vector<GemmProblem> host_problems;  // for inspection (roofline accounting)
+  NaryBatch fixup;              // deferred stream-K fixup launch (GemmSchedule::deferred)
   double flops = 0;             // 2*M*N*K summed
   double min_bytes = 0;         // operands read once + outputs written once
 };
@@ -137,9 +148,11 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream);
 // group count.
 // max_kb > 0 bounds every segment's k range (3xTF32 accuracy, see gemm.cu).
 GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int num_sms, int force_groups,
-                           int max_kb = 0);
+                           int max_kb = 0, bool deferred = false);
 void gemm_free(GemmLaunch& g);
 // Debug override of the MN-major descriptor strides (0 = defaults).
 void gemm_debug_mn_desc(unsigned lbo, unsigned sbo);
+// Debug (knob (22, 1)): the last traced launch's per-CTA timeline, 8 ns stamps per CTA.
+void gemm_debug_trace(unsigned long long* out, int n);
 
 }  // namespace tpx

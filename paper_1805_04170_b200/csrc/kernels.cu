@@ -88,7 +88,7 @@ __device__ __forceinline__ int find_desc(const int64_t* tile_begin_base, size_t 
 
 // Row tiling shared by nary / init: rows x inner (units) split into tiles of ~`tile` units.  A
 // tile is either a chunk of one long row (all threads on it) or rpt whole rows walked by groups
-// of rg threads (rg = 32..256, about 4 units per thread per row, so short rows still keep every
+// of rg threads (rg = 1..256, about 4 units per thread per row, so short rows still keep every
 // thread busy).
 struct RowTiling {
   int64_t rows, inner, rpt, col_chunk, n_col_chunks, rg;
@@ -106,7 +106,9 @@ RowTiling row_tiling(int64_t rows, int64_t inner, int64_t tile = kTileUnits) {
   } else {
     t.col_chunk = std::max<int64_t>(inner, 1);
     t.n_col_chunks = 1;
-    int64_t rg = 32;
+    // (short rows: fewer threads per row, down to one -- consecutive threads then take
+    // consecutive rows, so a tile of one-unit rows still keeps every lane busy)
+    int64_t rg = 1;
     while (rg < kThreads && rg * 4 < inner) rg *= 2;
     t.rg = rg;
     t.rpt = std::max<int64_t>(kThreads / rg, tile / t.col_chunk);

@@ -77,6 +77,7 @@ _SIGS = {
                           P(c_int), P(c_int), P(c_int), P(ctypes.c_int32), c_int,
                           P(ctypes.c_int32), c_int],
     "tpx_debug_gemm_mn_desc": [ctypes.c_uint, ctypes.c_uint],
+    "tpx_debug_gemm_trace": [P(c_u64), c_int],
     "tpx_gemm_last_launch": [P(c_i64), c_int],
 }
 
