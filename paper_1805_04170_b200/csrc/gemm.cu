@@ -507,12 +507,18 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     if constexpr (PAIR) tma_load_3d_pair(dst, map, bar_c, c0, c1, c2, pol);
     else tma_load_3d_hint(dst, map, bar, c0, c1, c2, pol);
   };
+  auto ld4 = [&](void* dst, const void* map, uint64_t* bar, uint32_t bar_c, int c2, int c3, uint64_t pol) {
+    if constexpr (PAIR) tma_load_4d_pair(dst, map, bar_c, 0, 0, c2, c3, pol);
+    else tma_load_4d_hint(dst, map, bar, 0, 0, c2, c3, pol);
+  };
   // bar: local barrier (single CTA); bar_c: the leader's barrier in the cluster window (pair)
   auto load_kblock = [&](const GemmProblem& pr, int kb, int p0, int q0, uint8_t* sa, uint8_t* sb,
                          uint64_t* bar, uint32_t bar_c, uint64_t pol_a, uint64_t pol_b) {
     const int ka = kb * BKE, kq = kb * BKE;
     if constexpr (!P_MN) {
       ld2(sa, pr.tmap_a, bar, bar_c, ka, p0, pol_a);
+    } else if (!BF16 && pr.a4d) {
+      ld4(sa, pr.tmap_a, bar, bar_c, p0 / MNC, ka / 4, pol_a);
     } else if (pr.a3d) {
       ld3(sa, pr.tmap_a, bar, bar_c, 0, ka, p0 / MNC, pol_a);
     } else {
@@ -521,6 +527,8 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
     }
     if constexpr (!Q_MN) {
       ld2(sb, pr.tmap_b, bar, bar_c, kq, q0, pol_b);
+    } else if (!BF16 && pr.b4d) {
+      ld4(sb, pr.tmap_b, bar, bar_c, q0 / MNC, kq / 4, pol_b);
     } else if (pr.b3d) {
       ld3(sb, pr.tmap_b, bar, bar_c, 0, kq, q0 / MNC, pol_b);
     } else {
@@ -593,16 +601,17 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
 #pragma unroll
         for (int kk = 0; kk < BKE / KPM; ++kk) {
           // K-major: 128B rows of K, 8-row atoms (SBO 1024), K step = +32 bytes.
-          // MN-major tf32: 128B rows of M/N per k, 32-byte-granule swizzle, 4-row groups
-          //   (SBO 512), 32-column chunks 4096 bytes apart (LBO), K step = 8 rows = +1024 bytes.
+          // MN-major tf32: 128B rows of M/N per k, 32-byte-granule swizzle, 512-byte atoms of
+          //   4 k rows x 32 columns; per-operand LBO (chunk stride), SBO (k-group stride) and K
+          //   step (8 rows = 2 k groups), GemmProblem::a_lbo ...
           // MN-major bf16: 128-byte swizzle, 8-row atoms (SBO 1024), 64-column chunks 8192 bytes
           //   apart (LBO), K step = 16 rows = +2048 bytes.
           const uint64_t ad = !P_MN ? umma_desc(sa + kk * 32, 16, 1024, 2)
                               : BF16 ? umma_desc(sa + kk * 2048, MNCH, 1024, 2)
-                                     : umma_desc(sa + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1);
+                                     : umma_desc(sa + kk * pr.a_kstep, pr.a_lbo, pr.a_sbo, 1);
           const uint64_t bd = !Q_MN ? umma_desc(sb + kk * 32, 16, 1024, 2)
                               : BF16 ? umma_desc(sb + kk * 2048, MNCH, 1024, 2)
-                                     : umma_desc(sb + kk * 1024, pr.mn_lbo, pr.mn_sbo, 1);
+                                     : umma_desc(sb + kk * pr.b_kstep, pr.b_lbo, pr.b_sbo, 1);
           const uint32_t accum = (kb > ck0 || kk > 0) ? 1u : 0u;
           if constexpr (SPLIT) {
             // low parts live OPB bytes after the high parts, in the same (swizzled) layout
@@ -1253,6 +1262,7 @@ int g_ts_chain = 0;    // debug (18, n): TMA-store epilogue also for chains (n =
 int g_trace = 0;       // debug (22, 1): per-CTA launch timeline (tpx_debug_gemm_trace)
 int g_whole = 0;       // debug (23, 1): whole tiles whenever there are no more tiles than groups
 int g_defer = 0;       // debug (24, 1): deferred stream-K fixup launch instead of in-kernel heads (measured slower: off)
+int g_mn4d = 1;       // debug (25, 0): MN-major tf32 operands in the chunk-major stage layout
 int g_rr_tiles = 1;    // debug (20, n): whole-tile schedules dealt round-robin (1, default) or in contiguous blocks (0)
 int g_tq_block = 0;    // debug (21, n): tile list in blocks of n Q-tiles (0 = Q-tile major)
 
@@ -1323,6 +1333,23 @@ void make_map_mn3d(CUtensorMap* m, const float* base, long long inner, long long
     throw std::runtime_error("cuTensorMapEncodeTiled (3-D) failed (" + std::to_string(int(r)) + ")");
 }
 
+// 4-D map of an MN-major tf32 operand (MN extent a multiple of 32, K a multiple of 4):
+// (32 MN elements, 4 k rows, MN/32 chunks, K/4 k groups); a box of (32, 4, nchunk, bke/4)
+// lands as bke/4 k groups, each holding its nchunk 512-byte atoms side by side.
+void make_map_mn4d(CUtensorMap* m, const float* base, long long inner, long long outer,
+                   long long row_stride, int nchunk, int bke) {
+  cuuint64_t dims[4] = {32, 4, (cuuint64_t)(inner / 32), (cuuint64_t)(outer / 4)};
+  const long long rs = std::max<long long>(row_stride, inner);
+  cuuint64_t strides[3] = {(cuuint64_t)(rs * 4), 128, (cuuint64_t)(rs * 16)};
+  cuuint32_t box[4] = {32, 4, (cuuint32_t)nchunk, (cuuint32_t)(bke / 4)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (4-D) failed (" + std::to_string(int(r)) + ")");
+}
+
 struct Role {
   const float* ptr;
   long long inner, outer, rs;
@@ -1364,9 +1391,10 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 22) g_trace = int(sbo);              // (22,1) launch timeline
   if (lbo == 23) g_whole = int(sbo);              // (23,1) whole tiles instead of stream-K
   if (lbo == 24) g_defer = int(sbo);              // (24,n) deferred stream-K fixup
+  if (lbo == 25) g_mn4d = int(sbo);               // (25,0) chunk-major MN-major stages
   if (lbo == 20) g_rr_tiles = int(sbo);           // (20,n) round-robin whole tiles
   if (lbo == 21) g_tq_block = int(sbo);           // (21,n) Q-tile blocks in the tile list
-  if (lbo >= 1 && lbo <= 24) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
+  if (lbo >= 1 && lbo <= 25) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1625,14 +1653,23 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
       throw std::runtime_error("gemm: mixed operand majorness in one batch");
     }
     GemmProblem& pr = probs[i];
-    if (rp.mn && rp.inner % mnc == 0 && !g_no_3d) {
+    auto mn4d_ok = [&](const Role& r) { return !bf && g_mn4d && r.mn && r.inner % 32 == 0 && r.outer % 4 == 0 && r.outer >= 4; };
+    if (mn4d_ok(rp)) {
+      make_map_mn4d(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, BM / 32, bke);
+      pr.a4d = 1;
+      pr.a_lbo = 512, pr.a_sbo = 512u * (BM / 32), pr.a_kstep = 2 * pr.a_sbo;
+    } else if (rp.mn && rp.inner % mnc == 0 && !g_no_3d) {
       make_map_mn3d(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, BM / mnc, bf);
       pr.a3d = 1;
     } else {
       make_map(&maps[2 * i], rp.ptr, rp.inner, rp.outer, rp.rs, rp.mn ? mnc : bke, rp.mn ? bke : BM, rp.mn,
                false, bf);
     }
-    if (rq.mn && rq.inner % mnc == 0 && !g_no_3d) {
+    if (mn4d_ok(rq)) {
+      make_map_mn4d(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, bnh / 32, bke);
+      pr.b4d = 1;
+      pr.b_lbo = 512, pr.b_sbo = 512u * (bnh / 32), pr.b_kstep = 2 * pr.b_sbo;
+    } else if (rq.mn && rq.inner % mnc == 0 && !g_no_3d) {
       make_map_mn3d(&maps[2 * i + 1], rq.ptr, rq.inner, rq.outer, rq.rs, bnh / mnc, bf);
       pr.b3d = 1;
     } else {
@@ -1648,8 +1685,8 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     pr.out = s.c;
     pr.out_rs = g.swap ? s.c_cs : s.c_rs;
     pr.out_cs = g.swap ? s.c_rs : s.c_cs;
-    if (g_dbg_lbo) pr.mn_lbo = g_dbg_lbo;
-    if (g_dbg_sbo) pr.mn_sbo = g_dbg_sbo;
+    if (g_dbg_lbo) pr.a_lbo = pr.b_lbo = g_dbg_lbo;
+    if (g_dbg_sbo) pr.a_sbo = pr.b_sbo = g_dbg_sbo;
     pr.n_epi = s.n_epi;
     for (int e = 0; e < s.n_epi; ++e) {
       pr.epi[e] = s.epi[e];

@@ -47,9 +47,17 @@ struct GemmProblem {
   long long out_rs = 0, out_cs = 0;
   int n_epi = 0;
   EpiStage epi[kMaxEpi];
-  unsigned mn_lbo = 4096, mn_sbo = 512;  // MN-major (128B_BASE32B) descriptor strides (bytes)
+  // MN-major tf32 (128B_BASE32B) descriptor strides per operand, bytes: LBO = between 32-wide
+  // MN chunks, SBO = between 4-row k groups, kstep = one MMA's 8 k rows.  Chunk-major stage
+  // (2-D / 3-D maps): 4096 / 512 / 1024; k-group-major stage (4-D maps): 512 / nchunk*512 / 2*SBO
+  unsigned a_lbo = 4096, a_sbo = 512, a_kstep = 1024;
+  unsigned b_lbo = 4096, b_sbo = 512, b_kstep = 1024;
   // MN-major operand mapped in 3-D (32-wide chunk, K, chunk index): one TMA op per k-block
   int a3d = 0, b3d = 0;
+  // MN-major tf32 operand mapped in 4-D (32-wide chunk, 4 k rows, chunk, k group): the stage
+  // holds each 4-row k group's chunks side by side (the layout CUTLASS tiles its SW128_32B atom
+  // to), one TMA op per k-block
+  int a4d = 0, b4d = 0;
   // L2 policy per operand (0 = evict_last: small and re-read by many tiles; 1 = evict_first:
   // streamed) and streaming (.cs) epilogue stores for outputs far larger than L2
   int a_stream = 0, b_stream = 0, out_stream = 0;
