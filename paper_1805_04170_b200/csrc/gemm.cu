@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   const int s_begin = dyn ? 0 : seg_off[unit], s_end = dyn ? seg_off[1] : seg_off[unit + 1];
   const int warp = warp_id(), lane = lane_id();
   const bool tr = (has_other >> 16) & 1;
+  const bool epf = ((has_other >> 17) & 1) == 0;  // TMEM chunk prefetch in the epilogue
   if (threadIdx.x == 0) trace_mark(tr, 0);
   if (warp == 3 && lane == 0 && !dyn && s_begin < s_end) {
     // the first segment's operand descriptors, fetched while the CTA sets up (a cold tensor map
@@ -806,17 +807,31 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
       ++ai;
       const bool have = sg.kb1 > sg.kb0;
       const uint32_t taddr = tmem_base + acc * BN + (uint32_t(lq * 32) << 16);
+      // TMEM chunk prefetch: the chunk loops take chunk c0 and issue c0 + CSTEP before the
+      // stores of c0, so the TMEM read latency hides behind the previous chunk's global traffic
+      uint32_t pf[CW];
+      auto pf_issue = [&](int c) {
+        if (have && c < c_end) tmem_ld16_issue(taddr + c, pf);
+      };
+      auto pf_take = [&](int c0, float (&v)[CW]) {
+        tmem_ld16_wait(pf);
+#pragma unroll
+        for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(pf[j]);
+        if (epf) pf_issue(c0 + CSTEP);
+        else if (c0 + CSTEP < c_end) tmem_ld16_issue(taddr + c0 + CSTEP, pf), tmem_ld16_wait(pf);
+      };
       if (has_other & 2) mbar_wait_sleep(&tmem_full[acc], aph);
       else mbar_wait(&tmem_full[acc], aph);
       if (ew == 0 && lane == 0 && ai == 1) trace_mark(tr, 5);
       tc_fence_after();
 
       if (sg.kind == SEG_PART) {
+        pf_issue(c_begin);
 #pragma unroll 1
         for (int c0 = c_begin; c0 < c_end; c0 += CSTEP) {
           float v[CW];
           if (have) {
-            tmem_ld16(taddr + c0, v);
+            pf_take(c0, v);
             add_sum(c0, v);
           } else {
 #pragma unroll
@@ -895,13 +910,14 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         const uint64_t spol = policy_evict_first();  // outputs far larger than L2 (ostream)
         const uint32_t box_w = smem_u32(out_stage) + uint32_t(ew * NBOX) * kOutStage;
         const bool dbl = NBOX >= 2 * nout;  // two box sets: chunk k+1 fills while k's stores read
+        pf_issue(c_begin);
 #pragma unroll 1
         for (int c0 = c_begin; c0 < c_end; c0 += CSTEP) {
           const int q0 = sg.tq * BN + c0;
           const uint32_t box0 = box_w + (dbl ? box_half * uint32_t(nout) * kOutStage : 0u);
           float v[CW], o[CW];
           if (have) {
-            tmem_ld16(taddr + c0, v);
+            pf_take(c0, v);
             add_sum(c0, v);
           } else {
 #pragma unroll
@@ -1007,12 +1023,13 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
         else if (n_epi == 2 && eop[0] == EPI_SCALE && eop[1] == EPI_SUB_OP && oe == 1) chain = 3;
         else if (n_epi == 2 && eop[0] == EPI_TANH && eop[1] == EPI_DTANH) chain = 4;
         const float s0 = esc[0];
+        pf_issue(c_begin);
 #pragma unroll 1
         for (int c0 = c_begin; c0 < c_end; c0 += CSTEP) {
           const int q0 = sg.tq * BN + c0;
           float v[CW];
           if (have) {
-            tmem_ld16(taddr + c0, v);
+            pf_take(c0, v);
             add_sum(c0, v);
           } else {
 #pragma unroll
@@ -1262,6 +1279,7 @@ int g_ts_chain = 0;    // debug (18, n): TMA-store epilogue also for chains (n =
 int g_trace = 0;       // debug (22, 1): per-CTA launch timeline (tpx_debug_gemm_trace)
 int g_whole = 0;       // debug (23, 1): whole tiles whenever there are no more tiles than groups
 int g_defer = 0;       // debug (24, 1): deferred stream-K fixup launch instead of in-kernel heads (measured slower: off)
+int g_epi_pf = 1;     // debug (26, 0): epilogue TMEM chunks loaded on demand, not one ahead
 int g_mn4d = 1;       // debug (25, 0): MN-major tf32 operands in the chunk-major stage layout
 int g_rr_tiles = 1;    // debug (20, n): whole-tile schedules dealt round-robin (1, default) or in contiguous blocks (0)
 int g_tq_block = 0;    // debug (21, n): tile list in blocks of n Q-tiles (0 = Q-tile major)
@@ -1391,10 +1409,11 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 22) g_trace = int(sbo);              // (22,1) launch timeline
   if (lbo == 23) g_whole = int(sbo);              // (23,1) whole tiles instead of stream-K
   if (lbo == 24) g_defer = int(sbo);              // (24,n) deferred stream-K fixup
+  if (lbo == 26) g_epi_pf = int(sbo);             // (26,0) no TMEM chunk prefetch
   if (lbo == 25) g_mn4d = int(sbo);               // (25,0) chunk-major MN-major stages
   if (lbo == 20) g_rr_tiles = int(sbo);           // (20,n) round-robin whole tiles
   if (lbo == 21) g_tq_block = int(sbo);           // (21,n) Q-tile blocks in the tile list
-  if (lbo >= 1 && lbo <= 25) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
+  if (lbo >= 1 && lbo <= 26) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1900,7 +1919,7 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair, g.bf16);
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
-  const int flags = (g_trace ? 1 << 16 : 0) | (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
+  const int flags = (g_trace ? 1 << 16 : 0) | (g_epi_pf ? 0 : 1 << 17) | (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
                     (g.other_smem && g.oloader && !g.sched.dynamic ? 2048 : 0) | (g.split ? (g_split_chain & 15) << 12 : 0);
   if (g.pair) {
     cudaLaunchConfig_t cfg = {};
