@@ -429,6 +429,8 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   const int warp = warp_id(), lane = lane_id();
   const bool tr = (has_other >> 16) & 1;
   const bool epf = ((has_other >> 17) & 1) == 0;  // TMEM chunk prefetch in the epilogue
+  const int nost = (has_other >> 18) & 7;          // debug: outputs whose stores are skipped
+  const int stag = (has_other >> 21) & 63;         // debug: start delay of odd units, us
   if (threadIdx.x == 0) trace_mark(tr, 0);
   if (warp == 3 && lane == 0 && !dyn && s_begin < s_end) {
     // the first segment's operand descriptors, fetched while the CTA sets up (a cold tensor map
@@ -540,6 +542,10 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
     const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+    // debug (28, us): odd units start that many microseconds late (phase offset between the
+    // units' store-heavy epilogues and their mainloops)
+    if (stag > 0 && (unit & 1))
+      for (int i = 0; i < stag; ++i) __nanosleep(1000);
     uint32_t s = 0, ph = 0;  // ring slot and its phase parity
     Cursor cur{0, s_begin, false};
     for (int j = 0;; ++j) {
@@ -1071,6 +1077,7 @@ __global__ void __launch_bounds__(threads_for(SPLIT), 1)
           // store stage e's values, then round them as stored (the next stage reads the stored
           // value, like the unfused launch would)
           auto put = [&](int e) {
+            if ((nost >> e) & 1) { round4<BF16>(x); return; }  // debug (27, mask): output e not stored
             const long long d0 = dofs[e] + q0;
             if (full_blk) {
 #pragma unroll
@@ -1279,6 +1286,8 @@ int g_ts_chain = 0;    // debug (18, n): TMA-store epilogue also for chains (n =
 int g_trace = 0;       // debug (22, 1): per-CTA launch timeline (tpx_debug_gemm_trace)
 int g_whole = 0;       // debug (23, 1): whole tiles whenever there are no more tiles than groups
 int g_defer = 0;       // debug (24, 1): deferred stream-K fixup launch instead of in-kernel heads (measured slower: off)
+int g_stagger = 0;    // debug (28, us): odd units start late
+int g_nostore = 0;    // debug (27, mask): fast-path epilogue skips the global stores of these outputs
 int g_epi_pf = 1;     // debug (26, 0): epilogue TMEM chunks loaded on demand, not one ahead
 int g_mn4d = 1;       // debug (25, 0): MN-major tf32 operands in the chunk-major stage layout
 int g_rr_tiles = 1;    // debug (20, n): whole-tile schedules dealt round-robin (1, default) or in contiguous blocks (0)
@@ -1409,11 +1418,13 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 22) g_trace = int(sbo);              // (22,1) launch timeline
   if (lbo == 23) g_whole = int(sbo);              // (23,1) whole tiles instead of stream-K
   if (lbo == 24) g_defer = int(sbo);              // (24,n) deferred stream-K fixup
+  if (lbo == 28) g_stagger = int(sbo);            // (28,us) odd units start late
+  if (lbo == 27) g_nostore = int(sbo);            // (27,mask) timing probe: outputs not stored
   if (lbo == 26) g_epi_pf = int(sbo);             // (26,0) no TMEM chunk prefetch
   if (lbo == 25) g_mn4d = int(sbo);               // (25,0) chunk-major MN-major stages
   if (lbo == 20) g_rr_tiles = int(sbo);           // (20,n) round-robin whole tiles
   if (lbo == 21) g_tq_block = int(sbo);           // (21,n) Q-tile blocks in the tile list
-  if (lbo >= 1 && lbo <= 26) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
+  if (lbo >= 1 && lbo <= 28) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1919,7 +1930,7 @@ void gemm_run(const GemmLaunch& g, cudaStream_t stream) {
   KernelFn fn = kernel_for(g.bn, g.p_mn, g.q_mn, g.split, g.pair, g.bf16);
   const GemmProblem* probs = static_cast<const GemmProblem*>(g.d_problems);
   const GemmSeg* segs = static_cast<const GemmSeg*>(g.d_segs);
-  const int flags = (g_trace ? 1 << 16 : 0) | (g_epi_pf ? 0 : 1 << 17) | (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
+  const int flags = (g_trace ? 1 << 16 : 0) | (g_epi_pf ? 0 : 1 << 17) | ((g_nostore & 7) << 18) | ((g_stagger & 63) << 21) | (g.other_smem ? 1 : 0) | (g_sleep ? 2 : 0) | (g.odepth << 4) | (g.sched.dynamic ? 128 : 0) | (g.nbox << 8) |
                     (g.other_smem && g.oloader && !g.sched.dynamic ? 2048 : 0) | (g.split ? (g_split_chain & 15) << 12 : 0);
   if (g.pair) {
     cudaLaunchConfig_t cfg = {};
