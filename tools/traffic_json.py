@@ -15,5 +15,7 @@ acc = {}
 for cls, row in zip(order, rows[2:]):
     b = float(row[ir]) * unit[rows[1][ir]] + float(row[iw]) * unit[rows[1][iw]]
     acc.setdefault(cls, []).append(b)
-out = {c: sum(v) / len(v) for c, v in acc.items()}
+src = (f"{rep} (ncu --set full --clock-control none -k regex:gemm, one cfg2 k=0 step, tools/ncu_step.py): "
+       "dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged per class")
+out = {c: {"dram_bytes_per_launch": sum(v) / len(v), "source": src} for c, v in acc.items()}  # bench.py reads this
 json.dump(out, sys.stdout, indent=1)
