@@ -1286,6 +1286,12 @@ int g_ts_chain = 0;    // debug (18, n): TMA-store epilogue also for chains (n =
 int g_trace = 0;       // debug (22, 1): per-CTA launch timeline (tpx_debug_gemm_trace)
 int g_whole = 0;       // debug (23, 1): whole tiles whenever there are no more tiles than groups
 int g_defer = 0;       // debug (24, 1): deferred stream-K fixup launch instead of in-kernel heads (measured slower: off)
+// Long-K tile width: the widest tile whose count still leaves each tile cut into at most this
+// many stream-K k-ranges, down to 128-wide tiles (the head sums the cut parts serially in its
+// epilogue; weight-streaming M = 128 x 8192 x 8192: 4.6 cuts of 256-wide tiles 76 us, 2.3 cuts of
+// 128-wide tiles 61 us)
+int g_max_cuts = 3;   // debug (30, n)
+int g_swap_below = 128;  // debug (29, n): compute the output transposed when M < n (and N >= 2M)
 int g_stagger = 0;    // debug (28, us): odd units start late
 int g_nostore = 0;    // debug (27, mask): fast-path epilogue skips the global stores of these outputs
 int g_epi_pf = 1;     // debug (26, 0): epilogue TMEM chunks loaded on demand, not one ahead
@@ -1418,13 +1424,15 @@ void gemm_debug_mn_desc(unsigned lbo, unsigned sbo) {
   if (lbo == 22) g_trace = int(sbo);              // (22,1) launch timeline
   if (lbo == 23) g_whole = int(sbo);              // (23,1) whole tiles instead of stream-K
   if (lbo == 24) g_defer = int(sbo);              // (24,n) deferred stream-K fixup
+  if (lbo == 30) g_max_cuts = std::max(1, int(sbo));  // (30,n) stream-K cuts per tile (width rule)
+  if (lbo == 29) g_swap_below = int(sbo);         // (29,n) swap threshold on M
   if (lbo == 28) g_stagger = int(sbo);            // (28,us) odd units start late
   if (lbo == 27) g_nostore = int(sbo);            // (27,mask) timing probe: outputs not stored
   if (lbo == 26) g_epi_pf = int(sbo);             // (26,0) no TMEM chunk prefetch
   if (lbo == 25) g_mn4d = int(sbo);               // (25,0) chunk-major MN-major stages
   if (lbo == 20) g_rr_tiles = int(sbo);           // (20,n) round-robin whole tiles
   if (lbo == 21) g_tq_block = int(sbo);           // (21,n) Q-tile blocks in the tile list
-  if (lbo >= 1 && lbo <= 28) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
+  if (lbo >= 1 && lbo <= 30) g_dbg_lbo = g_dbg_sbo = 0;  // (small lbo values are knobs, not strides)
 }
 
 bool gemm_view_ok(const MatView& v, bool bf16) {
@@ -1609,7 +1617,7 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
     if (s.bf16 != bf) throw std::runtime_error("gemm: mixed storage types in one batch");
   const long long M0 = s0.ta ? s0.a.cols : s0.a.rows;
   const long long N0 = s0.tb ? s0.b.rows : s0.b.cols;
-  g.swap = (M0 < 128 && N0 >= 2 * M0);
+  g.swap = (M0 < g_swap_below && N0 >= 2 * M0);
   const long long Q0 = g.swap ? M0 : N0;
   g.bn = Q0 <= 32 ? 32 : Q0 <= 64 ? 64 : Q0 <= 128 ? 128 : 256;
   // an MN-major bf16 Q operand is staged in 64-element (128-byte) chunks: BN >= 64
@@ -1636,14 +1644,23 @@ GemmLaunch gemm_prepare(const std::vector<GemmSpec>& specs, int num_sms, bool sp
       }
       return std::make_pair(t, pair ? num_sms / 2 : num_sms);
     };
-    int pick = g.bn;
-    for (int bn = g.bn; bn >= min_bn; bn /= 2) {
-      pick = bn;
-      const auto tu = tiles(bn);
-      const long long need = kb <= 16 ? tu.second : std::max(1, tu.second / 5);
-      if (tu.first >= need) break;
-    }
-    g.bn = pick;
+    auto widest = [&](int cuts) {
+      int pick = g.bn;
+      for (int bn = g.bn; bn >= min_bn; bn /= 2) {
+        pick = bn;
+        const auto tu = tiles(bn);
+        const long long need = kb <= 16 ? tu.second : std::max(1, tu.second / cuts);
+        if (tu.first >= need) break;
+      }
+      return pick;
+    };
+    // At most 5 cuts per tile. A single row of P tiles (weight streaming: M <= 128 against a
+    // wide weight) takes at most g_max_cuts while that keeps tiles >= 128 wide: its heads' serial
+    // partial sums are the launch's tail. Several P-tile rows (conv grad_weight: P = 256..384,
+    // operand-traffic bound) keep the wide tiles (128-wide: AlexNet-style conv step +0.6 ms).
+    const int pick5 = widest(5);
+    const long long p_ext = g.swap ? N0 : M0;
+    g.bn = p_ext <= BM ? std::max(widest(g_max_cuts), std::min(pick5, 128)) : pick5;
   }
   if (g_max_bn > 0) g.bn = std::max(min_bn, std::min(g.bn, g_max_bn));
   g.nprob = int(specs.size());
