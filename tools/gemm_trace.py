@@ -18,18 +18,20 @@ for arg in sys.argv[1:]:
     parts = arg.split(",")
     M, N, K, ta, tb = (int(x) for x in parts[:5])
     epi = [int(x) for x in parts[5].split(":")] if len(parts) > 5 else []
-    A = torch.rand((K, M) if ta else (M, K), device="cuda")
-    B = torch.rand((N, K) if tb else (K, N), device="cuda")
-    C = torch.empty(M, N, device="cuda")
-    W = torch.rand(M, N, device="cuda")
-    outs = [torch.empty(M, N, device="cuda") for _ in epi]
+    prec = int(os.environ.get("PREC", "0"))  # 2: bf16 storage
+    dt = torch.bfloat16 if prec == 2 else torch.float32
+    A = torch.rand((K, M) if ta else (M, K), device="cuda").to(dt)
+    B = torch.rand((N, K) if tb else (K, N), device="cuda").to(dt)
+    C = torch.empty(M, N, device="cuda", dtype=dt)
+    W = torch.rand(M, N, device="cuda").to(dt)
+    outs = [torch.empty(M, N, device="cuda", dtype=dt) for _ in epi]
     e = [(op, 0.01, W if op >= 4 else None, o) for op, o in zip(epi, outs)]
-    native.gemm(A, B, bool(ta), bool(tb), C, epi=e, warmup=3, iters=5)
+    native.gemm(A, B, bool(ta), bool(tb), C, epi=e, warmup=3, iters=5, precision=prec)
     L.tpx_debug_gemm_mn_desc(ctypes.c_uint(22), ctypes.c_uint(1))
     buf = (ctypes.c_uint64 * (320 * 8))()
     for i in range(320 * 8):
         buf[i] = 0
-    native.gemm(A, B, bool(ta), bool(tb), C, epi=e)
+    native.gemm(A, B, bool(ta), bool(tb), C, epi=e, precision=prec)
     torch.cuda.synchronize()
     L.tpx_debug_gemm_trace(buf, 320 * 8)
     L.tpx_debug_gemm_mn_desc(ctypes.c_uint(22), ctypes.c_uint(0))
