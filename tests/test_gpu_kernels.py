@@ -84,3 +84,42 @@ def test_gemm_dynamic_schedule(shape, epi):
                 assert torch.equal(a, b)
     finally:
         native.lib().tpx_debug_gemm_mn_desc(10, 1)
+
+
+# MN-major (transposed) TF32 operands: the k-group-major stage (4-D TMA map) when the MN extent
+# is a multiple of 32 and K a multiple of 4, else the chunk-major stage (3-D / 2-D maps).
+MN_SHAPES = [  # M, N, K, ta, tb
+    (256, 256, 4, True, False), (256, 512, 12, True, False), (384, 256, 36, True, False),
+    (512, 256, 100, True, True), (96, 640, 64, True, False), (256, 96, 64, False, False),
+    (256, 256, 30, True, False), (80, 256, 64, True, False), (256, 200, 64, False, False),
+    (2048, 2048, 512, True, False), (512, 2048, 2048, False, False),
+]
+
+
+@pytest.mark.parametrize("shape", MN_SHAPES, ids=lambda s: "x".join(map(str, s[:3])) + ("T" if s[3] else "N") + ("T" if s[4] else "N"))
+@pytest.mark.parametrize("precision", [0, 1], ids=["tf32", "fp32"])
+def test_mn_major_stage_layouts(shape, precision):
+    """Both MN-major stage layouts against torch fp64, and bit-identical to each other (the same
+    products in the same k order; only the shared-memory arrangement differs)."""
+    import ctypes
+
+    import torch
+    from paper_1805_04170_b200 import native
+    C, ref, _, _ = _run(*shape, precision)
+    assert _nw(C, ref) <= (2e-3 if precision == 0 else 1e-5)
+    native.lib().tpx_debug_gemm_mn_desc(ctypes.c_uint(25), ctypes.c_uint(0))  # chunk-major stages
+    try:
+        C0, _, _, _ = _run(*shape, precision)
+    finally:
+        native.lib().tpx_debug_gemm_mn_desc(ctypes.c_uint(25), ctypes.c_uint(1))
+    assert torch.equal(C, C0)
+
+
+def test_weight_streaming_tile_width():
+    """A single row of P tiles against a wide weight (the cfg2 per-GPU fwd shape at N = 4) takes
+    128-wide tiles (<= 3 stream-K cuts each, gemm.cu g_max_cuts) and stays exact."""
+    from paper_1805_04170_b200 import native
+    C, ref, _, _ = _run(128, 8192, 8192, False, False, 0)
+    info = native.last_launch()
+    assert (info["bn"], info["pair"], info["swap"], info["stream_k"]) == (128, 0, 0, 1)
+    assert _nw(C, ref) <= 2e-3
