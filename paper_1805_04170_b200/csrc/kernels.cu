@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "util.h"
@@ -686,8 +688,8 @@ __device__ __forceinline__ void im2col_body(const ConvDesc& d, int tile) {
   }
 }
 
-template <class T>
-__global__ void __launch_bounds__(kThreads, 4) col2im_kernel(const ConvDesc* __restrict__ ds, int n) {
+template <class T, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) col2im_kernel(const ConvDesc* __restrict__ ds, int n) {
   //   out[nb, c, y, x] = sum_{u,v} col[(c,u,v)*pitch + nb*img + (y-u)*Xo + (x-v)]
   //   (b.ptr != null: also writes 1 - tanh(out)^2 there, from the stored value)
   __shared__ long long ctoff[32];
@@ -819,8 +821,8 @@ __device__ __forceinline__ void transpose_body(const ConvDesc& d, int tile) {
   }
 }
 
-template <class T>
-__global__ void __launch_bounds__(kThreads) premove_kernel(const ConvDesc* __restrict__ ds, int n) {
+template <class T, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) premove_kernel(const ConvDesc* __restrict__ ds, int n) {
   const int di = find_desc(&ds[0].tile_begin, sizeof(ConvDesc), n, blockIdx.x);
   const ConvDesc& d = ds[di];
   const int tile = int(int64_t(blockIdx.x) - d.tile_begin);
@@ -1126,10 +1128,27 @@ void conv_run(const ConvBatch& b, cudaStream_t s) {
   const size_t sm = size_t(b.smem);
   const bool col2im = b.move && b.descs[0].mode == CONV_COL2IM;
 
-  if (col2im && b.bf16) col2im_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
-  else if (col2im) col2im_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
-  else if (b.move && b.bf16) premove_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, sm, s>>>(ds, nd);
-  else if (b.move) premove_kernel<float><<<unsigned(b.tiles), kThreads, sm, s>>>(ds, nd);
+  // register budget (min resident blocks per SM) of the data-movement kernels; debug override
+  // TPX_MOVE_MINB=<premove>,<col2im> for A/B runs
+  // (measured on the AlexNet-style conv step: premove 1 -> 4 blocks, im2col 1.67 -> 1.30 ms;
+  // col2im 4 -> 6 blocks, 2.00 -> 1.79 ms; 8 blocks spill and run 1.6x slower)
+  static int mb_pre = 4, mb_c2i = 6, mb_init = 0;
+  if (!mb_init) {
+    mb_init = 1;
+    if (const char* e = std::getenv("TPX_MOVE_MINB")) std::sscanf(e, "%d,%d", &mb_pre, &mb_c2i);
+  }
+  const unsigned g = unsigned(b.tiles);
+#define TPX_C2I(T) \
+  (mb_c2i >= 8 ? col2im_kernel<T, 8> : mb_c2i == 6 ? col2im_kernel<T, 6> : mb_c2i == 5 ? col2im_kernel<T, 5> \
+   : mb_c2i == 3 ? col2im_kernel<T, 3> : mb_c2i <= 2 ? col2im_kernel<T, 2> : col2im_kernel<T, 4>)
+#define TPX_PRE(T) \
+  (mb_pre >= 8 ? premove_kernel<T, 8> : mb_pre >= 6 ? premove_kernel<T, 6> : mb_pre >= 4 ? premove_kernel<T, 4> : premove_kernel<T, 1>)
+  if (col2im && b.bf16) TPX_C2I(__nv_bfloat16)<<<g, kThreads, 0, s>>>(ds, nd);
+  else if (col2im) TPX_C2I(float)<<<g, kThreads, 0, s>>>(ds, nd);
+  else if (b.move && b.bf16) TPX_PRE(__nv_bfloat16)<<<g, kThreads, sm, s>>>(ds, nd);
+  else if (b.move) TPX_PRE(float)<<<g, kThreads, sm, s>>>(ds, nd);
+#undef TPX_C2I
+#undef TPX_PRE
   else if (b.bf16) conv_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
   else conv_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, nd);
   CUDA_CHECK(cudaGetLastError());

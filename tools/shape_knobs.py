@@ -23,7 +23,8 @@ for ks in sys.argv[i + 1:] or ["base"]:
     for k, v in pairs:
         native.lib().tpx_debug_gemm_mn_desc(ctypes.c_uint(k), ctypes.c_uint(v))
     for (M, N, K, ta, tb), epi in shapes:
-        ms = statistics.median(bench(M, N, K, bool(ta), bool(tb), iters=20, epi=epi)[0] for _ in range(5))
+        prec = int(os.environ.get("PREC", "0"))  # 2: bf16 storage
+        ms = statistics.median(bench(M, N, K, bool(ta), bool(tb), iters=20, epi=epi, precision=prec)[0] for _ in range(5))
         info = native.last_launch()
         print(f"{name:10s} {(M, N, K, ta, tb)} epi={epi}: {ms * 1e3:7.1f} us  pair={info.get('pair')} bn={info.get('bn')} "
               f"sk={info.get('stream_k')} group={info.get('group')} stages={info.get('stages')}", flush=True)
