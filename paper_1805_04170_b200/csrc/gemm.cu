@@ -1454,7 +1454,10 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
   int G = 1;
   bool same_tp = true;
   for (const auto& pr : probs) same_tp = same_tp && pr.tiles_p == probs[0].tiles_p;
-  const double q_bytes = 4.0 * double(probs[0].Q) * double(probs[0].K);
+  // (the streamed bytes of the whole batch: 8 sub-problems of 32 MB weights are streamed from
+  // DRAM like one 256 MB weight -- tiled-on-one-GPU loop k3 fwd 0.16-0.20 ms with G = 1)
+  double q_bytes = 0;
+  for (const auto& pr : probs) q_bytes += 4.0 * double(pr.Q) * double(pr.K);
   if (same_tp && probs[0].tiles_p >= 2 && probs[0].tiles_p <= 8 && 2 * probs[0].tiles_p <= num_sms &&
       q_bytes > 32.0 * (1 << 20))
     G = probs[0].tiles_p;
