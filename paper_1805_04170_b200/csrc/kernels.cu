@@ -238,8 +238,8 @@ __device__ __forceinline__ float stored(float v) {
 
 // The block's descriptor, staged in shared memory once (a per-thread walk of the global
 // descriptor table costs dozens of dependent loads per block).
-template <class T>
-__global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
+template <class T, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) nary_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
                                                            PeerSync sync, int signal_s, int wait_s) {
   __shared__ __align__(16) unsigned char sraw[(sizeof(NaryDev) + 15) / 16 * 16];
   __shared__ int sdi;
@@ -380,8 +380,8 @@ __global__ void __launch_bounds__(kThreads, 2) nary_kernel(const NaryDev* __rest
 // Batches made only of plain box copies (pack / unpack / pull / concat pieces, no chain): one
 // source per descriptor, so a light kernel (few registers, full occupancy) with 8 independent
 // loads in flight per thread -- enough to cover NVLink latency on a peer read.
-template <class T>
-__global__ void __launch_bounds__(kThreads, 3) copy_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
+template <class T, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) copy_kernel(const NaryDev* __restrict__ ds, const int* __restrict__ tile_desc,
                                                            PeerSync sync, int signal_s, int wait_s) {
   __shared__ int sdi;
   if (threadIdx.x == 0) {
@@ -961,14 +961,27 @@ void nary_run(const NaryBatch& b, cudaStream_t s) {
   }
   const NaryDev* ds = static_cast<const NaryDev*>(b.d_descs);
   const int* td = static_cast<const int*>(b.d_tile_desc);
+  // register budgets (min resident blocks per SM); debug override TPX_NARY_MINB=<nary>,<copy>
+  // (copy 3 -> 4: cfg2 data k3 conversions 3.60 -> 3.51 ms, loop k3 0.219 -> 0.203 ms; 6 spills;
+  // nary 2 / 3 / 4 measured equal)
+  static int mb_nary = 2, mb_copy = 4, mb_init = 0;
+  if (!mb_init) {
+    mb_init = 1;
+    if (const char* e = std::getenv("TPX_NARY_MINB")) std::sscanf(e, "%d,%d", &mb_nary, &mb_copy);
+  }
+  const unsigned g = unsigned(b.tiles);
+#define TPX_COPY(T) (mb_copy >= 6 ? copy_kernel<T, 6> : mb_copy >= 4 ? copy_kernel<T, 4> : copy_kernel<T, 3>)
+#define TPX_NARY(T) (mb_nary >= 4 ? nary_kernel<T, 4> : mb_nary == 3 ? nary_kernel<T, 3> : nary_kernel<T, 2>)
   if (b.copy_only) {
-    if (b.bf16) copy_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
-    else copy_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
+    if (b.bf16) TPX_COPY(__nv_bfloat16)<<<g, kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
+    else TPX_COPY(float)<<<g, kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
     CUDA_CHECK(cudaGetLastError());
     return;
   }
-  if (b.bf16) nary_kernel<__nv_bfloat16><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
-  else nary_kernel<float><<<unsigned(b.tiles), kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
+  if (b.bf16) TPX_NARY(__nv_bfloat16)<<<g, kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
+  else TPX_NARY(float)<<<g, kThreads, 0, s>>>(ds, td, b.sync, b.signal_s, b.wait_s);
+#undef TPX_COPY
+#undef TPX_NARY
   CUDA_CHECK(cudaGetLastError());
 }
 
