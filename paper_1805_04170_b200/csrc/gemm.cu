@@ -1284,7 +1284,7 @@ int g_odepth = 0;      // debug (15, n): operand ring depth n (0 = chosen from t
 int g_min_stages = 4;  // debug (16, n): mainloop stages the operand ring must leave
 int g_ts_chain = 0;    // debug (18, n): TMA-store epilogue also for chains (n = 1 single, 2 double-buffered boxes)
 int g_trace = 0;       // debug (22, 1): per-CTA launch timeline (tpx_debug_gemm_trace)
-int g_whole = 0;       // debug (23, 1): whole tiles whenever there are no more tiles than groups
+int g_whole = 0;       // debug (23, 1): whole tiles whenever there are no more tiles than groups (default: when >= 80 % of the groups get one)
 int g_defer = 0;       // debug (24, 1): deferred stream-K fixup launch instead of in-kernel heads (measured slower: off)
 // Long-K tile width: the widest tile whose count still leaves each tile cut into at most this
 // many stream-K k-ranges, down to 128-wide tiles (the head sums the cut parts serially in its
@@ -1499,7 +1499,11 @@ GemmSchedule gemm_schedule(const std::vector<GemmProblem>& probs, int bn, int nu
   // fp32-accurate at any K (K = 8192: 4e-5 -> ~1e-6 normwise).
   bool chunked = false;
   for (const auto& c : cols) chunked = chunked || (max_kb > 0 && c.kb > max_kb);
-  const bool whole = !chunked && (ncols >= 8 * groups || ncols % groups == 0 || (g_whole && ncols <= groups));
+  // whole tiles also when every column fits on its own group and >= 80 % of the groups get one:
+  // no partial tiles, and the launch's tail is one epilogue (cfg2 fwd / bwd_x, 32 columns of 2
+  // pair tiles on 37 groups: 107 -> 104 us); fewer columns keep stream-K (long-K conv products)
+  const bool fill = ncols <= groups && (g_whole || 5LL * ncols >= 4LL * groups);
+  const bool whole = !chunked && (ncols >= 8 * groups || ncols % groups == 0 || fill);
   if (whole) groups = std::min(groups, ncols);
 
   // pieces[col] = ordered (group, kb0, kb1)

@@ -83,7 +83,11 @@ def test_schedule_baseline_shapes(shape):
 
 
 def test_small_m_groups_share_the_streamed_operand():
+    # 32 columns of 4 P-tiles on 37 groups: >= 80 % of the groups get a whole column
     S, _ = _check(1, 512, 8192, 8192, 256)
+    assert S["group"] == 4 and not S["stream_k"] and S["grid"] == 128
+    # 16 columns on 37 groups: stream-K, every CTA busy
+    S, _ = _check(1, 512, 4096, 8192, 256)
     assert S["group"] == 4 and S["stream_k"] and S["grid"] == 148
 
 
