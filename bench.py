@@ -417,10 +417,12 @@ def main():
     batch = workload_batch(args.config)
     prec = 1 if args.precision == "fp32" else 0  # bf16: storage type comes from the bf16 plan
     ctx = Context(local, rank, world)
-    if world > 1 and not peer:
+    if world > 1 and (not peer or not share):
+        # NCCL mode exchanges through this communicator; peer mode pulls over CUDA IPC and keeps
+        # it only as the stand-by route (ranks sharing one GPU cannot form one)
         ctx.init_comm_from_torch()
-        print(f"[bench] rank {rank}: NCCL communicator initialised (nranks={world}, device cuda:{local})",
-              file=sys.stderr, flush=True)
+        print(f"[bench] rank {rank}: NCCL communicator initialised (nranks={world}, device cuda:{local})"
+              + (" -- data path: peer pulls over NVLink (CUDA IPC)" if peer else ""), file=sys.stderr, flush=True)
     stream = torch.cuda.Stream()
     hbm_peak, bf16_peak, peak_kind = peaks()
     base_flags = FLAG_FUSE | FLAG_LOOP | (0 if args.no_graph else FLAG_GRAPH) | (FLAG_PEER if peer else 0)
