@@ -420,9 +420,15 @@ def main():
     if world > 1 and (not peer or not share):
         # NCCL mode exchanges through this communicator; peer mode pulls over CUDA IPC and keeps
         # it only as the stand-by route (ranks sharing one GPU cannot form one)
-        ctx.init_comm_from_torch()
-        print(f"[bench] rank {rank}: NCCL communicator initialised (nranks={world}, device cuda:{local})"
-              + (" -- data path: peer pulls over NVLink (CUDA IPC)" if peer else ""), file=sys.stderr, flush=True)
+        try:
+            ctx.init_comm_from_torch()
+            print(f"[bench] rank {rank}: NCCL communicator initialised (nranks={world}, device cuda:{local})"
+                  + (" -- data path: peer pulls over NVLink (CUDA IPC)" if peer else ""), file=sys.stderr, flush=True)
+        except Exception as e:  # noqa: BLE001
+            if not peer:
+                raise
+            print(f"[bench] rank {rank}: no NCCL communicator ({e}); peer mode does not need one",
+                  file=sys.stderr, flush=True)
     stream = torch.cuda.Stream()
     hbm_peak, bf16_peak, peak_kind = peaks()
     base_flags = FLAG_FUSE | FLAG_LOOP | (0 if args.no_graph else FLAG_GRAPH) | (FLAG_PEER if peer else 0)
