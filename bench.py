@@ -376,6 +376,11 @@ def main():
     import torch.distributed as dist
     from paper_1805_04170_b200.executor import (FLAG_FORCE_XCHG, FLAG_FUSE, FLAG_GRAPH, FLAG_LOOP, FLAG_PEER,
                                                 FLAG_PEER_SOLO, Context, PlanExecutor)
+    for kv in filter(None, os.environ.get("TPX_GEMM_KNOBS", "").split(",")):  # development A/B only
+        import ctypes
+        from paper_1805_04170_b200 import native
+        kk, vv = kv.split(":")
+        native.lib().tpx_debug_gemm_mn_desc(ctypes.c_uint(int(kk)), ctypes.c_uint(int(vv)))
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
